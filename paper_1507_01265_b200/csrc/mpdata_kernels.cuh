@@ -1,0 +1,57 @@
+// Launch interface of the sm_100a MPDATA kernels (host side of csrc/*.cu).
+// Every launcher returns the number of kernels it launched (for the
+// launch-count evidence) and never synchronises.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "recipe.cuh"
+
+namespace imb::dev {
+
+// A plane range [p0, p1) of a padded slab with m x l planes.
+struct Span {
+  std::int64_t m, l, p0, p1;
+};
+
+template <class T>
+int launch_update(const Span& s, const T* x, const T* U, const T* V, const T* W, const T* h,
+                  T* out, cudaStream_t st);
+template <class T>
+int launch_pseudo(const Span& s, const T* x, const T* U, const T* V, const T* W, const T* h,
+                  T* ut, T* vt, T* wt, cudaStream_t st);
+template <class T>
+int launch_bounds(const Span& s, const T* x, const T* xn, int first, T* mx, T* mn,
+                  cudaStream_t st);
+template <class T>
+int launch_beta(const Span& s, const T* x, const T* ut, const T* vt, const T* wt, const T* h,
+                const T* mx, const T* mn, T* bu, T* bd, cudaStream_t st);
+template <class T>
+int launch_limit(const Span& s, T* ut, T* vt, T* wt, const T* bu, const T* bd, cudaStream_t st);
+
+// Seeded recipe into the five padded-slab fields. Plane p holds global
+// i = (i0 + p - R) mod n, so halo planes are generated, not exchanged.
+template <class T>
+int launch_init(const recipe::Params& prm, std::int64_t i0, std::int64_t R, std::int64_t planes,
+                T* x, T* u, T* v, T* w, T* h, cudaStream_t st);
+
+// Reference surrogate stage ops on the padded GridField layout
+// (workload.hpp:66-74): 7-point max/min over the interior.
+int launch_stage7(const double* in, double* out, std::int64_t n, std::int64_t m, std::int64_t l,
+                  std::int64_t halo, bool is_max, cudaStream_t st);
+
+// ---- fused streaming step (csrc/mpdata_fused.cu) ----------------------
+struct FusedShape {
+  std::int64_t m, l;      // plane extents
+  std::int64_t ni, R;     // interior planes, halo planes of the padded slab
+  std::int64_t o0, o1;    // output plane range, local interior coordinates
+};
+// True when the fused kernel supports this (iord, nonos, m, l) combination.
+bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool fp64);
+template <class T>
+int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
+                 const T* w, const T* h, T* out, int num_sms, cudaStream_t st);
+
+}  // namespace imb::dev

@@ -1,0 +1,494 @@
+// GPU team runtime (team.hpp). Host C++; kernels live in csrc/*.cu.
+#include "team.hpp"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <utility>
+
+#include "imbalance/errors.hpp"
+
+namespace imb::rt {
+
+#define IMB_CUDA(call)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::imb::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " (" +      \
+                             __FILE__ + ":" + std::to_string(__LINE__) + ")");               \
+  } while (0)
+
+int step_radius(const Options& o) {
+  int r = 1;
+  for (int k = 2; k <= o.iord; ++k) r += o.nonos ? 2 : 1;
+  return r;
+}
+
+// ---- NCCL, loaded at run time so the library has no hard NCCL dependency --
+namespace {
+
+struct NcclApi {
+  void* dl = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      api.dl = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (api.dl) break;
+    }
+    if (!api.dl) return;
+    auto sym = [](const char* s) { return dlsym(api.dl, s); };
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(sym("ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(sym("ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+    api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+  });
+  if (!api.dl || !api.get_unique_id || !api.comm_init_rank || !api.send || !api.recv ||
+      !api.group_start || !api.group_end)
+    throw NcclError("NCCL (libnccl.so.2) could not be loaded");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    const char* msg = nccl().error_string ? nccl().error_string(r) : "?";
+    throw NcclError(std::string(what) + ": " + msg);
+  }
+}
+
+}  // namespace
+
+class NcclLink {
+ public:
+  NcclLink(const unsigned char* id, int nranks, int rank) : nranks_(nranks), rank_(rank) {
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, sizeof uid.internal);
+    nccl_check(nccl().comm_init_rank(&comm_, nranks, uid, rank), "ncclCommInitRank");
+  }
+  ~NcclLink() {
+    if (comm_ && nccl().comm_destroy) nccl().comm_destroy(comm_);
+  }
+  // Ring halo swap of R planes: my first planes go left, my last planes go
+  // right. Per-peer operations are matched in issue order, which keeps the
+  // two-rank ring (left == right) unambiguous.
+  void swap_halos(char* buf, std::size_t plane_bytes, std::int64_t R, std::int64_t ni,
+                  cudaStream_t st) {
+    const int left = (rank_ + nranks_ - 1) % nranks_, right = (rank_ + 1) % nranks_;
+    const std::size_t bytes = plane_bytes * static_cast<std::size_t>(R);
+    char* first = buf + plane_bytes * static_cast<std::size_t>(R);
+    char* last = buf + plane_bytes * static_cast<std::size_t>(ni);
+    char* halo_l = buf;
+    char* halo_r = buf + plane_bytes * static_cast<std::size_t>(R + ni);
+    nccl_check(nccl().group_start(), "ncclGroupStart");
+    nccl_check(nccl().send(first, bytes, ncclUint8, left, comm_, st), "ncclSend");
+    nccl_check(nccl().send(last, bytes, ncclUint8, right, comm_, st), "ncclSend");
+    nccl_check(nccl().recv(halo_r, bytes, ncclUint8, right, comm_, st), "ncclRecv");
+    nccl_check(nccl().recv(halo_l, bytes, ncclUint8, left, comm_, st), "ncclRecv");
+    nccl_check(nccl().group_end(), "ncclGroupEnd");
+  }
+  int nranks() const { return nranks_; }
+
+ private:
+  ncclComm_t comm_ = nullptr;
+  int nranks_, rank_;
+};
+
+void nccl_unique_id(unsigned char* out) {
+  ncclUniqueId uid;
+  nccl_check(nccl().get_unique_id(&uid), "ncclGetUniqueId");
+  std::memcpy(out, uid.internal, sizeof uid.internal);
+}
+
+// ---- Team -------------------------------------------------------------------
+Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, int device,
+           std::int64_t i0, std::int64_t ni)
+    : n_(n), m_(m), l_(l), opt_(opt), device_(device), i0_(i0), ni_(ni) {
+  if (n < 3 || m < 3 || l < 3) throw ContractError("grid extents must be >= 3");
+  if (opt.iord < 1 || opt.iord > 8) throw ConfigError("iord must be in [1, 8]");
+  if (i0 < 0 || i0 >= n || ni < 1 || ni > n) throw ContractError("slab outside the grid");
+  R_ = step_radius(opt);
+  if (ni < R_)
+    throw ContractError("slab of " + std::to_string(ni) + " planes is thinner than the step radius " +
+                        std::to_string(R_));
+  P_ = ni_ + 2 * R_;
+  int count = 0;
+  IMB_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    throw ConfigError("device " + std::to_string(device) + " not present (" +
+                      std::to_string(count) + " visible)");
+  IMB_CUDA(cudaSetDevice(device_));
+  IMB_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_));
+  IMB_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  IMB_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+  IMB_CUDA(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming));
+  IMB_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
+  const std::size_t fbytes = static_cast<std::size_t>(P_) * plane_bytes();
+  const bool fused = dev::fused_supported(opt_.iord, opt_.nonos, m_, l_, opt_.fp64) &&
+                     ni_ >= 2 * R_;
+  const int ntmp = fused ? 0 : 12;
+  const std::size_t total = fbytes * static_cast<std::size_t>(7 + ntmp);
+  if (cudaMalloc(&pool_, total) != cudaSuccess) {
+    cudaGetLastError();
+    throw ConfigError("cannot allocate " + std::to_string(total >> 20) + " MiB on device " +
+                      std::to_string(device_));
+  }
+  IMB_CUDA(cudaMemsetAsync(pool_, 0, total, cs_));
+  char* p = static_cast<char*>(pool_);
+  x_ = p;
+  xn_ = p + fbytes;
+  x0_ = p + 2 * fbytes;
+  for (int f = 0; f < 4; ++f) st_[f] = p + static_cast<std::size_t>(3 + f) * fbytes;
+  for (int t = 0; t < ntmp; ++t) tmp_[t] = p + static_cast<std::size_t>(7 + t) * fbytes;
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+}
+
+Team::~Team() {
+  cudaSetDevice(device_);
+  if (cs_) cudaStreamSynchronize(cs_);
+  if (xs_) cudaStreamSynchronize(xs_);
+  nccl_.reset();
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  if (ev_ready_) cudaEventDestroy(ev_ready_);
+  if (ev_halo_) cudaEventDestroy(ev_halo_);
+  if (cs_) cudaStreamDestroy(cs_);
+  if (xs_) cudaStreamDestroy(xs_);
+  if (pool_) cudaFree(pool_);
+  if (host_stage_) cudaFreeHost(host_stage_);
+}
+
+void* Team::fbuf(int field) const {
+  switch (field) {
+    case 0: return x_;
+    case 1: return st_[0];
+    case 2: return st_[1];
+    case 3: return st_[2];
+    case 4: return st_[3];
+    default: throw ContractError("field id must be 0..4 (x, u, v, w, h)");
+  }
+}
+
+void Team::init_recipe(int kind, std::uint64_t seed) {
+  if (kind < 0 || kind > 2) throw ConfigError("unknown recipe " + std::to_string(kind));
+  IMB_CUDA(cudaSetDevice(device_));
+  const recipe::Params prm = recipe::make_params(kind, n_, m_, l_, seed);
+  if (opt_.fp64)
+    launches_ += dev::launch_init<double>(prm, i0_, R_, P_, static_cast<double*>(x_),
+                                          static_cast<double*>(st_[0]), static_cast<double*>(st_[1]),
+                                          static_cast<double*>(st_[2]), static_cast<double*>(st_[3]), cs_);
+  else
+    launches_ += dev::launch_init<float>(prm, i0_, R_, P_, static_cast<float*>(x_),
+                                         static_cast<float*>(st_[0]), static_cast<float*>(st_[1]),
+                                         static_cast<float*>(st_[2]), static_cast<float*>(st_[3]), cs_);
+  IMB_CUDA(cudaGetLastError());
+  IMB_CUDA(cudaMemcpyAsync(x0_, x_, static_cast<std::size_t>(P_) * plane_bytes(),
+                           cudaMemcpyDeviceToDevice, cs_));
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+  static_halo_ok_ = true;  // recipe halos are generated, not exchanged
+}
+
+void Team::upload(int field, const void* host, std::size_t bytes) {
+  const std::size_t want = static_cast<std::size_t>(ni_) * plane_bytes();
+  if (bytes != want)
+    throw ContractError("upload of " + std::to_string(bytes) + " bytes, slab needs " +
+                        std::to_string(want));
+  IMB_CUDA(cudaSetDevice(device_));
+  char* dst = static_cast<char*>(fbuf(field)) + static_cast<std::size_t>(R_) * plane_bytes();
+  IMB_CUDA(cudaMemcpyAsync(dst, host, bytes, cudaMemcpyHostToDevice, cs_));
+  if (field == 0)
+    IMB_CUDA(cudaMemcpyAsync(static_cast<char*>(x0_) + static_cast<std::size_t>(R_) * plane_bytes(),
+                             dst, bytes, cudaMemcpyDeviceToDevice, cs_));
+  else
+    static_halo_ok_ = false;
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+}
+
+void Team::download(int field, void* host, std::size_t bytes) {
+  const std::size_t want = static_cast<std::size_t>(ni_) * plane_bytes();
+  if (bytes != want)
+    throw ContractError("download of " + std::to_string(bytes) + " bytes, slab holds " +
+                        std::to_string(want));
+  IMB_CUDA(cudaSetDevice(device_));
+  const char* src = static_cast<const char*>(fbuf(field)) + static_cast<std::size_t>(R_) * plane_bytes();
+  IMB_CUDA(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, cs_));
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+}
+
+void Team::reset() {
+  IMB_CUDA(cudaSetDevice(device_));
+  IMB_CUDA(cudaMemcpyAsync(x_, x0_, static_cast<std::size_t>(P_) * plane_bytes(),
+                           cudaMemcpyDeviceToDevice, cs_));
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+}
+
+// Periodic single slab: halo planes come from the opposite end of itself.
+void Team::exchange_x_self(void* buf) {
+  char* b = static_cast<char*>(buf);
+  const std::size_t pb = plane_bytes(), bytes = pb * static_cast<std::size_t>(R_);
+  IMB_CUDA(cudaMemcpyAsync(b, b + pb * static_cast<std::size_t>(ni_), bytes,
+                           cudaMemcpyDeviceToDevice, cs_));
+  IMB_CUDA(cudaMemcpyAsync(b + pb * static_cast<std::size_t>(R_ + ni_),
+                           b + pb * static_cast<std::size_t>(R_), bytes, cudaMemcpyDeviceToDevice, cs_));
+}
+
+void Team::exchange_x_nccl(void* buf) {
+  IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
+  IMB_CUDA(cudaStreamWaitEvent(xs_, ev_ready_, 0));
+  nccl_->swap_halos(static_cast<char*>(buf), plane_bytes(), R_, ni_, xs_);
+  IMB_CUDA(cudaEventRecord(ev_halo_, xs_));
+  IMB_CUDA(cudaStreamWaitEvent(cs_, ev_halo_, 0));
+}
+
+void Team::exchange_static() {
+  for (int f = 0; f < 4; ++f) {
+    if (nccl_ && nccl_->nranks() > 1)
+      exchange_x_nccl(st_[f]);
+    else
+      exchange_x_self(st_[f]);
+  }
+  static_halo_ok_ = true;
+}
+
+void Team::pull_from_ring(int field) {
+  const std::size_t pb = plane_bytes(), bytes = pb * static_cast<std::size_t>(R_);
+  char* mine = static_cast<char*>(fbuf(field));
+  const char* lsrc = static_cast<const char*>(left_->fbuf(field)) + pb * static_cast<std::size_t>(left_->ni_);
+  const char* rsrc = static_cast<const char*>(right_->fbuf(field)) + pb * static_cast<std::size_t>(right_->R_);
+  IMB_CUDA(cudaMemcpyPeerAsync(mine, device_, lsrc, left_->device_, bytes, cs_));
+  IMB_CUDA(cudaMemcpyPeerAsync(mine + pb * static_cast<std::size_t>(R_ + ni_), device_, rsrc,
+                               right_->device_, bytes, cs_));
+}
+
+void Team::begin_compute_window() {
+  if (ev_used_ + 2 > ev_pool_.size()) {
+    cudaEvent_t a, b;
+    IMB_CUDA(cudaEventCreate(&a));
+    IMB_CUDA(cudaEventCreate(&b));
+    ev_pool_.push_back(a);
+    ev_pool_.push_back(b);
+  }
+  IMB_CUDA(cudaEventRecord(ev_pool_[ev_used_], cs_));
+}
+
+void Team::end_compute_window() {
+  IMB_CUDA(cudaEventRecord(ev_pool_[ev_used_ + 1], cs_));
+  ev_used_ += 2;
+}
+
+double Team::take_compute_seconds() {
+  double s = 0.0;
+  if (ev_used_ > 0) IMB_CUDA(cudaEventSynchronize(ev_pool_[ev_used_ - 1]));
+  for (std::size_t q = 0; q + 1 < ev_used_; q += 2) {
+    float ms = 0.f;
+    IMB_CUDA(cudaEventElapsedTime(&ms, ev_pool_[q], ev_pool_[q + 1]));
+    s += static_cast<double>(ms) * 1e-3;
+  }
+  ev_used_ = 0;
+  return s;
+}
+
+namespace {
+struct Rng {
+  std::int64_t a, b;
+};
+Rng cap(Rng r, std::int64_t lo, std::int64_t hi) { return {std::max(r.a, lo), std::min(r.b, hi)}; }
+Rng hull(Rng x, Rng y) { return {std::min(x.a, y.a), std::max(x.b, y.b)}; }
+}  // namespace
+
+// One step on a halo-complete x: xn = MPDATA(x) on the interior, then swap.
+template <class T>
+void Team::compute_step_t() {
+  const T* x = static_cast<const T*>(x_);
+  const T* u = static_cast<const T*>(st_[0]);
+  const T* v = static_cast<const T*>(st_[1]);
+  const T* w = static_cast<const T*>(st_[2]);
+  const T* h = static_cast<const T*>(st_[3]);
+  T* out = static_cast<T*>(xn_);
+  if (tmp_[0] == nullptr) {
+    dev::FusedShape fs{m_, l_, ni_, R_, 0, ni_};
+    launches_ += dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h, out, num_sms_, cs_);
+    IMB_CUDA(cudaGetLastError());
+    std::swap(x_, xn_);
+    return;
+  }
+  T* it[2] = {static_cast<T*>(tmp_[0]), static_cast<T*>(tmp_[1])};
+  T* va[3] = {static_cast<T*>(tmp_[2]), static_cast<T*>(tmp_[3]), static_cast<T*>(tmp_[4])};
+  T* vb[3] = {static_cast<T*>(tmp_[5]), static_cast<T*>(tmp_[6]), static_cast<T*>(tmp_[7])};
+  T* mx = static_cast<T*>(tmp_[8]);
+  T* mn = static_cast<T*>(tmp_[9]);
+  T* bu = static_cast<T*>(tmp_[10]);
+  T* bd = static_cast<T*>(tmp_[11]);
+  const std::int64_t P = P_;
+  auto span = [&](Rng r) { return dev::Span{m_, l_, std::max<std::int64_t>(r.a, 1), std::min(r.b, P - 1)}; };
+  const Rng all{0, P};
+  const Rng goal{R_, R_ + ni_};
+  // Validity of every intermediate is tracked as a plane interval; each stage
+  // is launched on the widest interval its inputs support.
+  Rng rc{1, P - 1};
+  T* cur = (opt_.iord == 1) ? out : it[0];
+  launches_ += dev::launch_update<T>(span(opt_.iord == 1 ? goal : rc), x, u, v, w, h, cur, cs_);
+  if (opt_.iord == 1) {
+    IMB_CUDA(cudaGetLastError());
+    std::swap(x_, xn_);
+    return;
+  }
+  const T *U = u, *V = v, *W = w;
+  Rng ru = all, rvw = all, rm{0, 0};
+  T** vel = va;
+  int nit = 1;
+  for (int pass = 2; pass <= opt_.iord; ++pass) {
+    const Rng nu = {std::max({rc.a + 1, rvw.a + 1, ru.a}), std::min({rc.b, rvw.b, ru.b})};
+    const Rng nvw = {std::max({rc.a + 1, ru.a, rvw.a}), std::min({rc.b - 1, ru.b - 1, rvw.b})};
+    launches_ += dev::launch_pseudo<T>(span(hull(nu, nvw)), cur, U, V, W, h, vel[0], vel[1], vel[2], cs_);
+    Rng lu = nu, lvw = nvw;
+    if (opt_.nonos) {
+      const bool first = pass == 2;
+      const Rng nm = first ? Rng{rc.a + 1, rc.b - 1} : cap(Rng{rc.a + 1, rc.b - 1}, rm.a, rm.b);
+      launches_ += dev::launch_bounds<T>(span(nm), cur, x, first ? 1 : 0, mx, mn, cs_);
+      rm = nm;
+      const Rng nb = {std::max({rc.a + 1, nu.a, nvw.a, nm.a}), std::min({rc.b - 1, nu.b - 1, nvw.b, nm.b})};
+      launches_ += dev::launch_beta<T>(span(nb), cur, vel[0], vel[1], vel[2], h, mx, mn, bu, bd, cs_);
+      lu = {std::max(nu.a, nb.a + 1), std::min(nu.b, nb.b)};
+      lvw = {std::max(nvw.a, nb.a), std::min(nvw.b, nb.b)};
+      launches_ += dev::launch_limit<T>(span(hull(lu, lvw)), vel[0], vel[1], vel[2], bu, bd, cs_);
+    }
+    Rng nr = {std::max({rc.a + 1, lu.a, lvw.a}), std::min({rc.b - 1, lu.b - 1, lvw.b})};
+    T* dst;
+    if (pass == opt_.iord) {
+      if (nr.a > goal.a || nr.b < goal.b)
+        throw ContractError("internal: step radius does not cover the slab interior");
+      nr = goal;
+      dst = out;
+    } else {
+      dst = it[nit];
+      nit ^= 1;
+    }
+    launches_ += dev::launch_update<T>(span(nr), cur, vel[0], vel[1], vel[2], h, dst, cs_);
+    cur = dst;
+    rc = nr;
+    U = vel[0];
+    V = vel[1];
+    W = vel[2];
+    ru = lu;
+    rvw = lvw;
+    vel = (vel == va) ? vb : va;
+  }
+  IMB_CUDA(cudaGetLastError());
+  std::swap(x_, xn_);
+}
+
+void Team::compute_step() {
+  if (opt_.fp64)
+    compute_step_t<double>();
+  else
+    compute_step_t<float>();
+}
+
+void Team::run(int steps, double* compute_s, double* wall_s) {
+  if (steps < 0) throw ContractError("steps must be >= 0");
+  if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
+  IMB_CUDA(cudaSetDevice(device_));
+  const bool multi = nccl_ && nccl_->nranks() > 1;
+  cudaEvent_t t0, t1;
+  IMB_CUDA(cudaEventCreate(&t0));
+  IMB_CUDA(cudaEventCreate(&t1));
+  IMB_CUDA(cudaEventRecord(t0, cs_));
+  if (!static_halo_ok_) exchange_static();
+  ev_used_ = 0;
+  for (int s = 0; s < steps; ++s) {
+    if (multi)
+      exchange_x_nccl(x_);
+    else
+      exchange_x_self(x_);
+    begin_compute_window();
+    compute_step();
+    end_compute_window();
+  }
+  IMB_CUDA(cudaEventRecord(t1, cs_));
+  IMB_CUDA(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  IMB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  const double comp = take_compute_seconds();
+  if (compute_s) *compute_s = comp;
+  if (wall_s) *wall_s = static_cast<double>(ms) * 1e-3;
+}
+
+void Team::step_host(const void* x_in, void* x_out) {
+  if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
+  IMB_CUDA(cudaSetDevice(device_));
+  const std::size_t bytes = static_cast<std::size_t>(ni_) * plane_bytes();
+  char* interior = static_cast<char*>(x_) + static_cast<std::size_t>(R_) * plane_bytes();
+  IMB_CUDA(cudaMemcpyAsync(interior, x_in, bytes, cudaMemcpyHostToDevice, cs_));
+  if (!static_halo_ok_) exchange_static();
+  if (nccl_ && nccl_->nranks() > 1)
+    exchange_x_nccl(x_);
+  else
+    exchange_x_self(x_);
+  compute_step();
+  interior = static_cast<char*>(x_) + static_cast<std::size_t>(R_) * plane_bytes();
+  IMB_CUDA(cudaMemcpyAsync(x_out, interior, bytes, cudaMemcpyDeviceToHost, cs_));
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+}
+
+std::uint64_t Team::checksum() {
+  std::vector<unsigned char> host(static_cast<std::size_t>(ni_) * plane_bytes());
+  download(0, host.data(), host.size());
+  std::uint64_t hsh = 0xcbf29ce484222325ull;
+  for (unsigned char b : host) {
+    hsh ^= b;
+    hsh *= 0x100000001b3ull;
+  }
+  return hsh;
+}
+
+void Team::connect_nccl(const unsigned char* id, int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("bad NCCL rank/size");
+  IMB_CUDA(cudaSetDevice(device_));
+  nccl_ = std::make_unique<NcclLink>(id, nranks, rank);
+  if (nranks > 1) static_halo_ok_ = static_halo_ok_ && true;
+}
+
+void Team::group_mark_ready() {
+  IMB_CUDA(cudaSetDevice(device_));
+  IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
+}
+
+void Team::group_pull() {
+  IMB_CUDA(cudaSetDevice(device_));
+  IMB_CUDA(cudaStreamWaitEvent(cs_, left_->ev_ready_, 0));
+  IMB_CUDA(cudaStreamWaitEvent(cs_, right_->ev_ready_, 0));
+  if (!static_halo_ok_) {
+    for (int f = 1; f <= 4; ++f) pull_from_ring(f);
+    static_halo_ok_ = true;
+  }
+  pull_from_ring(0);
+}
+
+void Team::group_compute() {
+  IMB_CUDA(cudaSetDevice(device_));
+  begin_compute_window();
+  compute_step();
+  end_compute_window();
+}
+
+}  // namespace imb::rt

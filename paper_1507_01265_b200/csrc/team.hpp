@@ -1,0 +1,110 @@
+// GPU team runtime: one Team owns one i-slab of the periodic global grid on
+// one device — the B200 counterpart of imb::TeamRunner
+// (/root/reference/proj/include/imbalance/workload.hpp:94-122), where a team
+// of CPU threads becomes one GPU. It owns the padded-slab device buffers,
+// a compute stream and a communication stream, and one of three halo
+// exchangers: itself (periodic single slab), an in-process ring of teams
+// (device copies; also the P-slabs-on-one-GPU test backend), or NCCL
+// send/recv between processes (one process per GPU).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "mpdata_kernels.cuh"
+
+namespace imb::rt {
+
+struct Options {
+  int iord = 2;
+  int nonos = 1;
+  bool fp64 = true;
+};
+
+int step_radius(const Options& o);
+
+class NcclLink;  // defined in team.cpp
+
+class Team {
+ public:
+  Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, int device,
+       std::int64_t i0, std::int64_t ni);
+  ~Team();
+  Team(const Team&) = delete;
+  Team& operator=(const Team&) = delete;
+
+  void init_recipe(int kind, std::uint64_t seed);
+  void upload(int field, const void* host, std::size_t bytes);
+  void download(int field, void* host, std::size_t bytes);
+  void reset();
+  void run(int steps, double* compute_s, double* wall_s);
+  void step_host(const void* x_in, void* x_out);
+  std::uint64_t checksum();
+
+  void connect_nccl(const unsigned char* id, int nranks, int rank);
+  // In-process ring wiring (imb_group): neighbours own the adjacent slabs.
+  void set_ring(Team* left, Team* right) {
+    left_ = left;
+    right_ = right;
+  }
+
+  // Group stepping, issued by imb_group in three host phases per step, each
+  // phase over all teams before the next: (1) record "x of this step is
+  // complete", (2) wait for both neighbours and pull their edge planes into
+  // the halos, (3) compute and swap. Phase 2 reads the neighbours' current
+  // x buffers, so it must precede every phase-3 swap of the step.
+  void group_mark_ready();
+  void group_pull();
+  void group_compute();
+
+  std::int64_t launches() const { return launches_; }
+  int device() const { return device_; }
+  std::int64_t ni() const { return ni_; }
+  std::int64_t i0() const { return i0_; }
+  std::int64_t radius() const { return R_; }
+  cudaStream_t stream() const { return cs_; }
+  cudaEvent_t ready_event() const { return ev_ready_; }
+  double take_compute_seconds();
+  std::size_t elem() const { return opt_.fp64 ? 8 : 4; }
+
+ private:
+  void exchange_static();
+  void exchange_x_self(void* x);
+  void exchange_x_nccl(void* x);
+  void pull_from_ring(int field_buf);
+  void compute_step();  // x (halo-complete) -> xn, then swap
+  template <class T>
+  void compute_step_t();
+  void* fbuf(int field) const;
+  std::size_t plane_bytes() const { return static_cast<std::size_t>(m_ * l_) * elem(); }
+  void begin_compute_window();
+  void end_compute_window();
+
+  std::int64_t n_, m_, l_;
+  Options opt_;
+  int device_;
+  std::int64_t i0_, ni_, R_, P_;
+  int num_sms_ = 148;
+  cudaStream_t cs_ = nullptr, xs_ = nullptr;  // compute, exchange
+  cudaEvent_t ev_ready_ = nullptr, ev_halo_ = nullptr;
+  std::vector<cudaEvent_t> ev_pool_;  // begin/end pairs of compute windows
+  std::size_t ev_used_ = 0;
+  // device buffers (padded slabs of P_ planes)
+  void* pool_ = nullptr;
+  void* x_ = nullptr;
+  void* xn_ = nullptr;
+  void* x0_ = nullptr;
+  void* st_[4] = {nullptr, nullptr, nullptr, nullptr};  // u, v, w, h
+  void* tmp_[12] = {};  // iterates, 2 velocity sets, mx, mn, bu, bd
+  bool static_halo_ok_ = false;
+  std::int64_t launches_ = 0;
+  Team* left_ = nullptr;
+  Team* right_ = nullptr;
+  std::unique_ptr<NcclLink> nccl_;
+  void* host_stage_ = nullptr;  // pinned staging for step_host
+};
+
+}  // namespace imb::rt
