@@ -109,6 +109,16 @@ enum { IMB_NCCL_ID_BYTES = 128 };
 int imb_nccl_unique_id(unsigned char id[IMB_NCCL_ID_BYTES]);
 int imb_team_connect_nccl(imb_team* t, const unsigned char id[IMB_NCCL_ID_BYTES], int nranks,
                           int rank);
+/* The 4 point-to-point operations a rank issues per step (in order):
+ * kinds[q] 0 = send / 1 = recv, peers[q], and the plane range
+ * [first_plane[q], first_plane[q] + planes[q]) of the padded slab
+ * (ni interior planes + R halo planes on each side). Host-only; the NCCL
+ * exchange executes exactly this plan. */
+int imb_ring_plan(int rank, int nranks, int64_t ni, int64_t R, int kinds[4], int peers[4],
+                  int64_t first_plane[4], int64_t planes[4]);
+/* Slab offsets = exclusive prefix sums of the shares, in processor order
+ * (the decomposition of SURVEY.md §8a-12). */
+int imb_slab_offsets(const int64_t* shares, int p, int64_t* offsets);
 
 /* ---- in-process group of teams (the fake multi-GPU backend / one host
  * thread per GPU): slabs from `shares` in ring order, exchange by device

@@ -194,6 +194,35 @@ int imb_team_connect_nccl(imb_team* t, const unsigned char id[IMB_NCCL_ID_BYTES]
   });
 }
 
+int imb_ring_plan(int rank, int nranks, int64_t ni, int64_t R, int* kinds, int* peers,
+                  int64_t* first_plane, int64_t* planes) {
+  return guard([&] {
+    need(kinds, "kinds");
+    need(peers, "peers");
+    need(first_plane, "first_plane");
+    need(planes, "planes");
+    imb::rt::RingOp ops[4];
+    imb::rt::ring_plan(rank, nranks, ni, R, ops);
+    for (int q = 0; q < 4; ++q) {
+      kinds[q] = ops[q].kind;
+      peers[q] = ops[q].peer;
+      first_plane[q] = ops[q].first_plane;
+      planes[q] = ops[q].planes;
+    }
+  });
+}
+
+int imb_slab_offsets(const int64_t* shares, int p, int64_t* offsets) {
+  return guard([&] {
+    need(shares, "shares");
+    need(offsets, "offsets");
+    if (p < 1) throw imb::ContractError("share list is empty");
+    const std::vector<std::int64_t> off =
+        imb::slab_offsets(std::span<const std::int64_t>(shares, static_cast<std::size_t>(p)));
+    std::copy(off.begin(), off.end(), offsets);
+  });
+}
+
 // ---- groups ------------------------------------------------------------------
 int imb_group_create(const imb_domain* global, const imb_opts* opts, int nteams,
                      const int* devices, const int64_t* shares, imb_group** out) {

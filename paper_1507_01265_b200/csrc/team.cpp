@@ -28,6 +28,16 @@ int step_radius(const Options& o) {
   return r;
 }
 
+void ring_plan(int rank, int nranks, std::int64_t ni, std::int64_t R, RingOp out[4]) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("bad ring rank/size");
+  if (ni < R || R < 1) throw ContractError("slab thinner than the halo");
+  const int left = (rank + nranks - 1) % nranks, right = (rank + 1) % nranks;
+  out[0] = RingOp{0, left, R, R};        // first interior planes -> left neighbour
+  out[1] = RingOp{0, right, ni, R};      // last interior planes -> right neighbour
+  out[2] = RingOp{1, right, R + ni, R};  // right halo <- right neighbour
+  out[3] = RingOp{1, left, 0, R};        // left halo <- left neighbour
+}
+
 // ---- NCCL, loaded at run time so the library has no hard NCCL dependency --
 namespace {
 
@@ -87,22 +97,20 @@ class NcclLink {
   ~NcclLink() {
     if (comm_ && nccl().comm_destroy) nccl().comm_destroy(comm_);
   }
-  // Ring halo swap of R planes: my first planes go left, my last planes go
-  // right. Per-peer operations are matched in issue order, which keeps the
-  // two-rank ring (left == right) unambiguous.
+  // Ring halo swap of R planes following ring_plan(), as one NCCL group.
   void swap_halos(char* buf, std::size_t plane_bytes, std::int64_t R, std::int64_t ni,
                   cudaStream_t st) {
-    const int left = (rank_ + nranks_ - 1) % nranks_, right = (rank_ + 1) % nranks_;
-    const std::size_t bytes = plane_bytes * static_cast<std::size_t>(R);
-    char* first = buf + plane_bytes * static_cast<std::size_t>(R);
-    char* last = buf + plane_bytes * static_cast<std::size_t>(ni);
-    char* halo_l = buf;
-    char* halo_r = buf + plane_bytes * static_cast<std::size_t>(R + ni);
+    RingOp plan[4];
+    ring_plan(rank_, nranks_, ni, R, plan);
     nccl_check(nccl().group_start(), "ncclGroupStart");
-    nccl_check(nccl().send(first, bytes, ncclUint8, left, comm_, st), "ncclSend");
-    nccl_check(nccl().send(last, bytes, ncclUint8, right, comm_, st), "ncclSend");
-    nccl_check(nccl().recv(halo_r, bytes, ncclUint8, right, comm_, st), "ncclRecv");
-    nccl_check(nccl().recv(halo_l, bytes, ncclUint8, left, comm_, st), "ncclRecv");
+    for (const RingOp& op : plan) {
+      char* p = buf + plane_bytes * static_cast<std::size_t>(op.first_plane);
+      const std::size_t bytes = plane_bytes * static_cast<std::size_t>(op.planes);
+      if (op.kind == 0)
+        nccl_check(nccl().send(p, bytes, ncclUint8, op.peer, comm_, st), "ncclSend");
+      else
+        nccl_check(nccl().recv(p, bytes, ncclUint8, op.peer, comm_, st), "ncclRecv");
+    }
     nccl_check(nccl().group_end(), "ncclGroupEnd");
   }
   int nranks() const { return nranks_; }

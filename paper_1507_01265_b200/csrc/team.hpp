@@ -26,6 +26,20 @@ struct Options {
 
 int step_radius(const Options& o);
 
+// One point-to-point operation of the per-step ring halo swap.
+struct RingOp {
+  int kind;                  // 0 = send, 1 = recv
+  int peer;                  // rank in the slab ring
+  std::int64_t first_plane;  // plane offset inside the padded slab
+  std::int64_t planes;       // number of contiguous planes
+};
+// The 4-operation plan every rank issues, in this order, each step: send
+// my first R interior planes left, my last R right, receive the right halo
+// from the right, the left halo from the left. Operations to one peer are
+// matched in issue order, so the two-rank ring (left == right) pairs
+// first->right-halo and last->left-halo correctly.
+void ring_plan(int rank, int nranks, std::int64_t ni, std::int64_t R, RingOp out[4]);
+
 class NcclLink;  // defined in team.cpp
 
 class Team {

@@ -132,6 +132,23 @@ class Team:
         check(load().imb_team_connect_nccl(self._h, uid, int(nranks), int(rank)))
 
 
+def ring_plan(rank: int, nranks: int, ni: int, R: int):
+    """The per-step halo-swap plan the NCCL exchange executes:
+    [(kind 'send'|'recv', peer, first_plane, planes)] in issue order."""
+    kinds, peers = (C.c_int * 4)(), (C.c_int * 4)()
+    first, planes = (C.c_int64 * 4)(), (C.c_int64 * 4)()
+    check(load().imb_ring_plan(int(rank), int(nranks), int(ni), int(R), kinds, peers, first,
+                               planes))
+    return [("send" if kinds[q] == 0 else "recv", peers[q], first[q], planes[q]) for q in range(4)]
+
+
+def slab_offsets(shares) -> list:
+    arr = (C.c_int64 * max(len(shares), 1))(*shares)
+    out = (C.c_int64 * max(len(shares), 1))()
+    check(load().imb_slab_offsets(arr, len(shares), out))
+    return list(out[:len(shares)])
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(load().imb_nccl_unique_id(buf))

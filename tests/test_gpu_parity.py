@@ -1,0 +1,182 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the CPU oracle on the
+same seeded inputs (BASELINE.json north_star tolerance: max relative error
+1e-12 in fp64, 1e-5 in fp32; relative error floored at |ref| >= 1 per
+SURVEY.md App. C #7), plus size-independent properties at full size."""
+import numpy as np
+import pytest
+
+from paper_1507_01265_b200 import _lib, mpdata
+from paper_1507_01265_b200.mpdata import Group, Options, Team
+
+pytestmark = pytest.mark.gpu
+
+TOL = {True: 1e-12, False: 1e-5}
+
+
+def rel_err(a, b):
+    return float(np.max(np.abs(a.astype(np.float64) - b.astype(np.float64)) /
+                        np.maximum(np.abs(b.astype(np.float64)), 1.0)))
+
+
+def gpu_run(fields, opts, steps):
+    n, m, l = fields[0].shape
+    with Team(n, m, l, opts) as t:
+        t.upload_all(*fields)
+        t.run(steps)
+        assert t.launches > 0
+        return t.download("x")
+
+
+def oracle_run(orc, fields, opts, steps):
+    return orc.run(*fields, iord=opts.iord, nonos=opts.nonos, steps=steps, threads=8)
+
+
+def test_config1_parity(orc):
+    # BASELINE config 1: 64x64x32 fp64, periodic, 10 steps, IORD=2, nonos off.
+    opts = Options(iord=2, nonos=False, fp64=True)
+    f = orc.init_fields(1, 64, 64, 32, seed=42)
+    got = gpu_run(f, opts, 10)
+    want = oracle_run(orc, f, opts, 10)
+    assert rel_err(got, want) <= 1e-12
+    assert want.min() < 1.5  # the divergent config exercises |psi| ratios
+
+
+def test_config2_parity(orc):
+    # BASELINE config 2: 256x256x64 fp64, 50 steps, IORD=2, limiter on.
+    opts = Options(iord=2, nonos=True, fp64=True)
+    f = orc.init_fields(2, 256, 256, 64, seed=42)
+    got = gpu_run(f, opts, 50)
+    want = oracle_run(orc, f, opts, 50)
+    assert rel_err(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+@pytest.mark.parametrize("iord,nonos", [(1, False), (2, False), (2, True), (3, True), (3, False)])
+@pytest.mark.parametrize("recipe", [0, 2])
+def test_scheme_matrix_parity(orc, fp64, iord, nonos, recipe):
+    opts = Options(iord=iord, nonos=nonos, fp64=fp64)
+    dt = np.float64 if fp64 else np.float32
+    f = orc.init_fields(recipe, 24, 20, 36, seed=5, dtype=dt)
+    got = gpu_run(f, opts, 4)
+    want = oracle_run(orc, f, opts, 4)
+    assert rel_err(got, want) <= TOL[fp64]
+
+
+@pytest.mark.parametrize("shape", [(5, 3, 3), (7, 33, 65), (16, 129, 20), (40, 8, 256)])
+def test_ragged_shapes_parity(orc, shape):
+    opts = Options(iord=3, nonos=True, fp64=True)
+    f = orc.init_fields(0, *shape, seed=17)
+    got = gpu_run(f, opts, 3)
+    want = oracle_run(orc, f, opts, 3)
+    assert rel_err(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+@pytest.mark.parametrize("recipe", [0, 2])
+def test_device_init_is_bit_identical_to_host(orc, fp64, recipe):
+    dt = np.float64 if fp64 else np.float32
+    n, m, l = 20, 12, 10
+    want = orc.init_fields(recipe, n, m, l, seed=99, dtype=dt)
+    with Team(n, m, l, Options(fp64=fp64), i0=6, ni=9) as t:
+        t.init_recipe(recipe, 99)
+        for name, ref in zip("xuvwh", want):
+            np.testing.assert_array_equal(t.download(name), ref[6:15])
+
+
+@pytest.mark.parametrize("shares", [[16, 16], [10, 6, 16], [3, 29], [8, 8, 8, 8], [11, 21]])
+@pytest.mark.parametrize("opts", [Options(2, True, True), Options(3, True, False),
+                                  Options(2, False, True)])
+def test_group_decomposition_is_bit_identical(shares, opts):
+    # P slabs on one GPU exchanging halos by device copies must reproduce the
+    # single-slab result exactly: the per-cell arithmetic is identical, so
+    # any difference is a halo/indexing bug.
+    n, m, l = sum(shares), 24, 40
+    R = mpdata.step_radius(opts)
+    if min(shares) < R:
+        pytest.skip("slab thinner than the step radius")
+    with Team(n, m, l, opts) as t:
+        t.init_recipe(2, 7)
+        t.run(5)
+        single = t.download("x")
+    g = Group(n, m, l, shares, opts=opts)
+    g.init_recipe(2, 7)
+    per, wall = g.run(5)
+    assert len(per) == len(shares) and wall > 0
+    np.testing.assert_array_equal(g.download("x"), single)
+    g.close()
+
+
+def test_group_with_uploaded_fields(orc):
+    opts = Options(2, True, True)
+    f = orc.init_fields(0, 30, 16, 24, seed=3)
+    g = Group(30, 16, 24, [12, 18], opts=opts)
+    off = 0
+    for t in g.teams:
+        t.upload_all(*(a[off:off + t.ni] for a in f))
+        off += t.ni
+    g.run(3)
+    want = oracle_run(orc, f, opts, 3)
+    assert rel_err(g.download("x"), want) <= 1e-12
+    g.close()
+
+
+def test_step_host_matches_run_and_reset(orc):
+    opts = Options(2, True, True)
+    f = orc.init_fields(2, 32, 24, 16, seed=1)
+    with Team(32, 24, 16, opts) as t:
+        t.upload_all(*f)
+        xin = np.ascontiguousarray(f[0])
+        xout = np.empty_like(xin)
+        t.step_host(xin, xout)
+        t.reset()
+        t.run(1)
+        np.testing.assert_array_equal(t.download("x"), xout)
+        c1 = t.checksum()
+        t.reset()
+        t.run(1)
+        assert t.checksum() == c1
+    assert rel_err(xout, oracle_run(orc, f, opts, 1)) <= 1e-12
+
+
+def test_stage_max7_min7_on_gpu(orc):
+    import ctypes as C
+    n, m, l, h = 8, 9, 10, 1
+    rng = np.random.default_rng(3)
+    f = orc.fill_halo_clamped(rng.random((n + 2, m + 2, l + 2)), n, m, l, h)
+    lib = _lib.load()
+    d = _lib.imb_domain(n, m, l, h)
+    P = C.POINTER(C.c_double)
+    for is_max, fn in ((True, lib.imb_stage_max7), (False, lib.imb_stage_min7)):
+        out = np.zeros_like(f)
+        _lib.check(fn(C.byref(d), f.ctypes.data_as(P), out.ctypes.data_as(P)))
+        want = orc.stage7(f, n, m, l, h, is_max)
+        np.testing.assert_array_equal(out[1:-1, 1:-1, 1:-1], want[1:-1, 1:-1, 1:-1])
+
+
+def test_contract_errors_on_gpu():
+    with pytest.raises(_lib.ContractError):
+        Team(16, 8, 8, Options(3, True), i0=0, ni=4)  # slab thinner than R=5
+    with pytest.raises(_lib.ContractError):
+        Group(16, 8, 8, [8, 7])  # shares must sum to n
+    with pytest.raises(_lib.ConfigError):
+        Team(16, 8, 8, Options(2, True), device=64)
+    with Team(16, 8, 8) as t:
+        with pytest.raises(_lib.ContractError):
+            t.upload("x", np.zeros((15, 8, 8)))
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+def test_full_size_properties(fp64):
+    # BASELINE config 4 grid (1024x512x128): mass conservation and the
+    # limiter's bounds hold at full size (size-independent parity checks).
+    opts = Options(2, True, fp64)
+    with Team(1024, 512, 128, opts) as t:
+        t.init_recipe(2, 42)
+        x0 = t.download("x").astype(np.float64)
+        h = t.download("h").astype(np.float64)
+        m0 = float(np.sum(h * x0))
+        t.run(3)
+        x = t.download("x").astype(np.float64)
+    tol = 1e-12 if fp64 else 1e-5
+    assert abs(float(np.sum(h * x)) - m0) <= tol * m0
+    assert x.min() >= x0.min() - 1e-3 and x.max() <= x0.max() + 1e-3
