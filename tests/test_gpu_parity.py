@@ -180,3 +180,33 @@ def test_full_size_properties(fp64):
     tol = 1e-12 if fp64 else 1e-5
     assert abs(float(np.sum(h * x)) - m0) <= tol * m0
     assert x.min() >= x0.min() - 1e-3 and x.max() <= x0.max() + 1e-3
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+@pytest.mark.parametrize("nonos", [True, False])
+@pytest.mark.parametrize("shape", [(6, 5, 32), (17, 13, 64), (12, 40, 128), (9, 3, 128),
+                                   (30, 29, 32)])
+def test_fused_kernel_parity(orc, fp64, nonos, shape):
+    # Shapes with l in {32, 64, 128} take the fused streaming kernel; m not a
+    # multiple of the j-tile and m smaller than the tile exercise the wrap.
+    opts = Options(iord=2, nonos=nonos, fp64=fp64)
+    dt = np.float64 if fp64 else np.float32
+    f = orc.init_fields(2 if nonos else 1, *shape, seed=23, dtype=dt)
+    got = gpu_run(f, opts, 3)
+    want = oracle_run(orc, f, opts, 3)
+    assert rel_err(got, want) <= TOL[fp64]
+
+
+@pytest.mark.parametrize("shares", [[16, 16], [9, 7, 16], [6, 26], [8, 8, 8, 8]])
+@pytest.mark.parametrize("opts", [Options(2, True, True), Options(2, False, False)])
+def test_group_decomposition_fused_is_bit_identical(shares, opts):
+    n, m, l = sum(shares), 20, 64
+    with Team(n, m, l, opts) as t:
+        t.init_recipe(2, 7)
+        t.run(4)
+        single = t.download("x")
+    g = Group(n, m, l, shares, opts=opts)
+    g.init_recipe(2, 7)
+    g.run(4)
+    np.testing.assert_array_equal(g.download("x"), single)
+    g.close()
