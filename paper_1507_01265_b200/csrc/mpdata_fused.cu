@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "mpdata_kernels.cuh"
 #include "mpdata_math.cuh"
@@ -32,16 +33,16 @@ namespace imb::dev {
 
 namespace {
 
-template <class T, int L, int RW, int NW, bool NONOS>
+template <class T, int L, int RR_, int NT_, bool NONOS>
 struct Cfg {
-  static constexpr int KPL = L / 32;              // k values per lane
-  static constexpr int Q = RW * KPL;              // cells per thread
-  static constexpr int RR = NW * RW;              // region rows
+  static constexpr int RR = RR_;                  // region rows
+  static constexpr int Q = RR * L / NT_;          // cells per thread
+  static_assert(Q * NT_ == RR * L && NT_ % L == 0, "threads must tile whole rows");
   static constexpr int HALO = NONOS ? 2 : 1;      // recomputed rows on each side
   static constexpr int TJ = RR - 2 * HALO;        // output rows per tile
-  static constexpr int NT = NW * 32;
+  static constexpr int NT = NT_;
   static constexpr int PLANE = RR * L;            // cells of one smem plane
-  static constexpr int NSLOT = NONOS ? 9 : 5;
+  static constexpr int NSLOT = NONOS ? 11 : 5;
   static constexpr std::size_t SMEM = sizeof(T) * PLANE * NSLOT;
 };
 
@@ -61,11 +62,40 @@ struct Args {
   long long plane;  // m * l
 };
 
-// Division flavours: exact IEEE in fp64, fast reciprocal in fp32.
-__device__ __forceinline__ double rcp(double a) { return 1.0 / a; }
-__device__ __forceinline__ float rcp(float a) { return __frcp_rn(a); }
-__device__ __forceinline__ double qdiv(double a, double b) { return a / b; }
-__device__ __forceinline__ float qdiv(float a, float b) { return __fdividef(a, b); }
+// Reciprocals without the IEEE-division slow path: fp64 = MUFU.RCP64H seed +
+// two Newton steps (error ~2^-80 before the final rounding, i.e. within an
+// ulp); fp32 = MUFU.RCP (~1 ulp). Arguments are positive and normal here
+// (denominators carry +eps, densities are positive).
+__device__ __forceinline__ double rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ float rcp(float d) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
+  return y;
+}
+__device__ __forceinline__ double qdiv(double a, double b) { return a * rcp(b); }
+__device__ __forceinline__ float qdiv(float a, float b) { return a * rcp(b); }
+
+// Upwind flux c * (c > 0 ? a : b): equal to pos(c) a + neg(c) b exactly.
+template <class T>
+__device__ __forceinline__ T upflux(T a, T b, T c) {
+  return c * (c > T(0) ? a : b);
+}
+// Limited velocity: vel * min(1, bdL, buR) for outflow to the right, else
+// vel * min(1, buL, bdR) — equal to dev::limit exactly.
+template <class T>
+__device__ __forceinline__ T limit_sel(T vel, T bdL, T buR, T buL, T bdR) {
+  const bool right = vel > T(0);
+  const T a = right ? bdL : buL;
+  const T b = right ? buR : bdR;
+  return vel * tmin(tmin(T(1), a), b);
+}
 
 // Pseudo-velocity at one face with a single reciprocal:
 //   ((|U| hb - U^2) nA dB dC - 0.125 U (S1 nB dC + S2 nC dB) dA) / (hb dA dB dC)
@@ -94,17 +124,18 @@ __device__ __forceinline__ T pseudo_face(T Un, T hL, T hR, T aR, T aL, T bp, T b
   }
 }
 
-template <class T, int L, int RW, int NW, bool NONOS>
-__global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RW, NW, NONOS>;
-  constexpr int Q = C::Q, KPL = C::KPL, RR = C::RR, PL = C::PLANE;
+template <class T, int L, int RR_, int NT, bool NONOS>
+__global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
+  using C = Cfg<T, L, RR_, NT, NONOS>;
+  constexpr int Q = C::Q, RR = C::RR, PL = C::PLANE;
+  constexpr int RSTEP = NT / L;  // rows between a thread's consecutive cells
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  T* s_x1 = sm;                 // 3 slots of psi^(1)
-  T* s_v = sm + 3 * PL;         // y-face pseudo-velocity slots
-  T* s_w = s_v + (NONOS ? 2 : 1) * PL;
-  T* s_bu = s_w + (NONOS ? 2 : 1) * PL;  // beta up   (NONOS)
-  T* s_bd = s_bu + PL;                   // beta down (NONOS)
+  T* s_x1 = sm;                          // 3 slots of psi^(1), by plane mod 3
+  T* s_v = sm + 3 * PL;                  // y-face pseudo-velocities
+  T* s_w = s_v + (NONOS ? 2 : 1) * PL;   // z-face pseudo-velocities
+  T* s_bu = s_w + (NONOS ? 2 : 1) * PL;  // beta up,   2 slots (NONOS)
+  T* s_bd = s_bu + 2 * PL;               // beta down, 2 slots (NONOS)
 
   const int tile = blockIdx.x % a.ntj;
   const int seg = blockIdx.x / a.ntj;
@@ -114,32 +145,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   if (ib >= ie) return;
   const int j0 = tile * C::TJ;
   const int m = a.m;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // Per-row global offsets (j wraps periodically); k and smem offsets are
-  // recomputed from (warp, lane, q) — q is a compile-time index.
-  int gjr[RW], gjmr[RW], gjpr[RW];
+  // Thread -> cells: cell q is (row r0 + q*RSTEP, column k); a warp covers 32
+  // consecutive k of one row, so every row test below is warp-uniform.
+  const int r0 = threadIdx.x / L, kc = threadIdx.x % L;
+  int gjr[Q], gjmr[Q], gjpr[Q];
 #pragma unroll
-  for (int rr = 0; rr < RW; ++rr) {
-    int j = j0 - C::HALO + warp * RW + rr;
+  for (int rr = 0; rr < Q; ++rr) {
+    int j = j0 - C::HALO + r0 + rr * RSTEP;
     j = ((j % m) + m) % m;
     gjr[rr] = j * L;
     gjmr[rr] = (j == 0 ? m - 1 : j - 1) * L;
     gjpr[rr] = (j == m - 1 ? 0 : j + 1) * L;
   }
 #define IMB_CELL(q)                                                   \
-  const int rr_ = (q) / KPL, kk_ = (q) % KPL;                         \
-  const int r = warp * RW + rr_;                                      \
-  const int k = lane + 32 * kk_;                                      \
+  const int rr_ = (q);                                                \
+  const int r = r0 + rr_ * RSTEP;                                     \
+  const int k = kc;                                                   \
   const int km = k == 0 ? L - 1 : k - 1, kp = k == L - 1 ? 0 : k + 1; \
   const int o = r * L + k, om_k = r * L + km, op_k = r * L + kp;      \
   const int gj = gjr[rr_], gjm = gjmr[rr_], gjp = gjpr[rr_];          \
   (void)om_k; (void)op_k; (void)gjm; (void)gjp; (void)km; (void)kp;
-#define IMB_CELL_END
-  auto slot3 = [](int p) { return ((p % 3) + 3) % 3; };
-  auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };  // plane offset
+  auto slot3 = [](int p) { return (p + 6) % 3; };  // p >= -3
+  auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
 
-  // ---- stage bodies -------------------------------------------------------
+  // ψn star extrema of the newest donor plane (NONOS), carried one plane.
+  T nmx_new[Q], nmn_new[Q], nmx[Q], nmn[Q];
   // P1: psi^(1) at plane p (donor cell) for all region rows.
   auto stage_donor = [&](int p) {
     const T* X = a.x + pl(p);
@@ -156,20 +186,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       IMB_CELL(q)
       const int c = gj + k;
       const T xc = __ldg(X + c);
-      const T fxl = flux(__ldg(Xm + c), xc, __ldg(U + c));
-      const T fxr = flux(xc, __ldg(Xp + c), __ldg(Up + c));
-      const T fyl = flux(__ldg(X + gjm + k), xc, __ldg(V + c));
-      const T fyr = flux(xc, __ldg(X + gjp + k), __ldg(V + gjp + k));
-      const T fzl = flux(__ldg(X + gj + km), xc, __ldg(W + c));
-      const T fzr = flux(xc, __ldg(X + gj + kp), __ldg(W + gj + kp));
+      const T xm = __ldg(Xm + c), xp = __ldg(Xp + c);
+      const T ym = __ldg(X + gjm + k), yp = __ldg(X + gjp + k);
+      const T zm = __ldg(X + gj + km), zp = __ldg(X + gj + kp);
+      const T fxl = upflux(xm, xc, __ldg(U + c));
+      const T fxr = upflux(xc, xp, __ldg(Up + c));
+      const T fyl = upflux(ym, xc, __ldg(V + c));
+      const T fyr = upflux(xc, yp, __ldg(V + gjp + k));
+      const T fzl = upflux(zm, xc, __ldg(W + c));
+      const T fzr = upflux(xc, zp, __ldg(W + gj + kp));
       const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-      dst[o] = xc - div / __ldg(H + c);
+      dst[o] = xc - qdiv(div, __ldg(H + c));
+      if constexpr (NONOS) {
+        nmx_new[q] = tmax(tmax(tmax(xc, xm), tmax(xp, ym)), tmax(tmax(yp, zm), zp));
+        nmn_new[q] = tmin(tmin(tmin(xc, xm), tmin(xp, ym)), tmin(tmin(yp, zm), zp));
+      }
     }
   };
 
-  // P2: pseudo-velocities around base plane pb: x-face pb+1 (returned in ut),
-  // y/z faces of plane pb (smem), and (NONOS) the bounds mx/mn of plane pb.
-  auto stage_pseudo = [&](int pb, bool only_u, T* ut, T* vdst, T* wdst, T* mxq, T* mnq) {
+  // P2: pseudo-velocities around base plane pb: x-face pb+1 (into ut), y and
+  // z faces of plane pb (into smem).
+  auto stage_pseudo = [&](int pb, bool only_u, T* ut, T* vdst, T* wdst) {
     const T* s0 = s_x1 + slot3(pb - 1) * PL;
     const T* s1 = s_x1 + slot3(pb) * PL;
     const T* s2 = s_x1 + slot3(pb + 1) * PL;
@@ -185,9 +222,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     for (int q = 0; q < Q; ++q) {
       IMB_CELL(q)
       const int c = gj + k;
-      const bool row_u = r >= 1 && r < RR - 1;   // x/z faces and bounds
-      const bool row_v = r >= 1;                 // y faces
+      const bool row_u = r >= 1 && r < RR - 1;  // x/z faces
+      const bool row_v = r >= 1;                // y faces
       const T a1c = fabs(s1[o]);
+      const T u2c = __ldg(U2 + c), h1c = __ldg(H1 + c);
       if (row_u) {  // x-face between planes pb and pb+1 of this column
         const T a2c = fabs(s2[o]);
         const T bp = fabs(s1[o + L]) + fabs(s2[o + L]);
@@ -197,10 +235,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const int cjp = gjp + k, ckp = gj + kp;
         const T Vs = (__ldg(V1 + c) + __ldg(V2 + c)) + (__ldg(V1 + cjp) + __ldg(V2 + cjp));
         const T Ws = (__ldg(W1 + c) + __ldg(W2 + c)) + (__ldg(W1 + ckp) + __ldg(W2 + ckp));
-        ut[q] = pseudo_face<T>(__ldg(U2 + c), __ldg(H1 + c), __ldg(H2 + c), a2c, a1c, bp, bm, Vs,
-                               cp, cm, Ws);
+        ut[q] = pseudo_face<T>(u2c, h1c, __ldg(H2 + c), a2c, a1c, bp, bm, Vs, cp, cm, Ws);
       }
       if (only_u) continue;
+      const T u1c = __ldg(U1 + c);
       if (row_v) {  // y-face between rows r-1 and r of plane pb
         const int om = o - L;
         const int cjm = gjm + k;
@@ -209,11 +247,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const T bm = fabs(s0[om]) + fabs(s0[o]);
         const T cp = fabs(s1[op_k - L]) + fabs(s1[op_k]);
         const T cm = fabs(s1[om_k - L]) + fabs(s1[om_k]);
-        const T Us = (__ldg(U1 + cjm) + __ldg(U1 + c)) + (__ldg(U2 + cjm) + __ldg(U2 + c));
+        const T Us = (__ldg(U1 + cjm) + u1c) + (__ldg(U2 + cjm) + u2c);
         const int cjmkp = gjm + kp, ckp = gj + kp;
         const T Ws = (__ldg(W1 + cjm) + __ldg(W1 + c)) + (__ldg(W1 + cjmkp) + __ldg(W1 + ckp));
-        vdst[o] = pseudo_face<T>(__ldg(V1 + c), __ldg(H1 + cjm), __ldg(H1 + c), a1c, aL, bp, bm,
-                                 Us, cp, cm, Ws);
+        vdst[o] = pseudo_face<T>(__ldg(V1 + c), __ldg(H1 + cjm), h1c, a1c, aL, bp, bm, Us, cp, cm,
+                                 Ws);
       }
       if (row_u) {  // z-face between k-1 and k
         const int ckm = gj + km;
@@ -222,42 +260,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const T bm = fabs(s0[om_k]) + fabs(s0[o]);
         const T cp = fabs(s1[om_k + L]) + fabs(s1[o + L]);
         const T cm = fabs(s1[om_k - L]) + fabs(s1[o - L]);
-        const T Us = (__ldg(U1 + ckm) + __ldg(U1 + c)) + (__ldg(U2 + ckm) + __ldg(U2 + c));
+        const T Us = (__ldg(U1 + ckm) + u1c) + (__ldg(U2 + ckm) + u2c);
         const int cjpkm = gjp + km, cjp = gjp + k;
         const T Vs = (__ldg(V1 + ckm) + __ldg(V1 + c)) + (__ldg(V1 + cjpkm) + __ldg(V1 + cjp));
-        wdst[o] = pseudo_face<T>(__ldg(W1 + c), __ldg(H1 + ckm), __ldg(H1 + c), a1c, aL, bp, bm,
-                                 Us, cp, cm, Vs);
-        if constexpr (NONOS) {
-          // 7-point bounds over psi^(1) and psi^n at plane pb.
-          const T* X = a.x + pl(pb);
-          T hi = s1[o], lo = s1[o];
-          const T nb1[6] = {s0[o], s2[o], s1[o - L], s1[o + L], s1[om_k], s1[op_k]};
-          const T nbn[7] = {__ldg(X + c),           __ldg(a.x + pl(pb - 1) + c),
-                            __ldg(a.x + pl(pb + 1) + c), __ldg(X + gjm + k),
-                            __ldg(X + gjp + k),   __ldg(X + ckm),
-                            __ldg(X + gj + kp)};
-#pragma unroll
-          for (int e = 0; e < 6; ++e) {
-            hi = fmax(hi, nb1[e]);
-            lo = fmin(lo, nb1[e]);
-          }
-#pragma unroll
-          for (int e = 0; e < 7; ++e) {
-            hi = fmax(hi, nbn[e]);
-            lo = fmin(lo, nbn[e]);
-          }
-          mxq[q] = hi;
-          mnq[q] = lo;
-        }
+        wdst[o] = pseudo_face<T>(__ldg(W1 + c), __ldg(H1 + ckm), h1c, a1c, aL, bp, bm, Us, cp, cm,
+                                 Vs);
       }
     }
   };
 
-  // ---- register carries (same (j,k) column, previous plane) ----------------
-  T ucar[Q], ufresh[Q], fxc[Q], buc[Q], bdc[Q], bun[Q], bdn[Q], mxq[Q], mnq[Q];
+  // ---- register carries along i (same (j,k) column) -------------------------
+  T ucar[Q], ufresh[Q], fxc[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
-    ucar[q] = ufresh[q] = fxc[q] = buc[q] = bdc[q] = bun[q] = bdn[q] = mxq[q] = mnq[q] = T(0);
+    ucar[q] = ufresh[q] = fxc[q] = T(0);
+    nmx[q] = nmn[q] = nmx_new[q] = nmn_new[q] = T(0);
   }
 
   const int lag = NONOS ? 2 : 1;  // psi^(1) planes ahead of the output plane
@@ -265,8 +282,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // pseudo-velocity between them.
   stage_donor(ib - lag);
   stage_donor(ib - lag + 1);
+  if constexpr (NONOS) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      nmx[q] = nmx_new[q];
+      nmn[q] = nmn_new[q];
+    }
+  }
   __syncthreads();
-  stage_pseudo(ib - lag, true, ucar, nullptr, nullptr, nullptr, nullptr);
+  stage_pseudo(ib - lag, true, ucar, nullptr, nullptr);
 
   const int tstart = NONOS ? ib - 2 : ib;
   for (int t = tstart; t < ie; ++t) {
@@ -275,13 +299,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     __syncthreads();
     if constexpr (NONOS) {
       const int p1 = t + 1;
-      T* vA = s_v + (p1 & 1) * PL;          // y-face velocities of plane t+1
+      T* vA = s_v + (p1 & 1) * PL;              // y-face velocities, plane t+1
       T* wA = s_w + (p1 & 1) * PL;
       const T* vB = s_v + ((p1 + 1) & 1) * PL;  // limited, plane t
       const T* wB = s_w + ((p1 + 1) & 1) * PL;
-      stage_pseudo(p1, false, ufresh, vA, wA, mxq, mnq);
+      T* buA = s_bu + (p1 & 1) * PL;            // beta, plane t+1
+      T* bdA = s_bd + (p1 & 1) * PL;
+      const T* buB = s_bu + ((p1 + 1) & 1) * PL;  // beta, plane t
+      const T* bdB = s_bd + ((p1 + 1) & 1) * PL;
+      stage_pseudo(p1, false, ufresh, vA, wA);
       __syncthreads();
-      // P3: beta bounds of plane t+1.
+      // P3: 7-point bounds and beta of plane t+1.
       {
         const T* s0 = s_x1 + slot3(t) * PL;
         const T* s1 = s_x1 + slot3(t + 1) * PL;
@@ -292,29 +320,35 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           IMB_CELL(q)
           if (r < 1 || r >= RR - 1) continue;
           const T xc = s1[o];
-          const T axl = flux(s0[o], xc, ucar[q]);
-          const T axr = flux(xc, s2[o], ufresh[q]);
-          const T ayl = flux(s1[o - L], xc, vA[o]);
-          const T ayr = flux(xc, s1[o + L], vA[o + L]);
-          const T azl = flux(s1[om_k], xc, wA[o]);
-          const T azr = flux(xc, s1[op_k], wA[op_k]);
-          const T fin = ((pos(axl) - neg(axr)) + (pos(ayl) - neg(ayr))) + (pos(azl) - neg(azr));
-          const T fout = ((pos(axr) - neg(axl)) + (pos(ayr) - neg(ayl))) + (pos(azr) - neg(azl));
+          const T xm = s0[o], xp = s2[o], ym = s1[o - L], yp = s1[o + L];
+          const T zm = s1[om_k], zp = s1[op_k];
+          const T mx = tmax(tmax(tmax(nmx[q], xc), tmax(xm, xp)), tmax(tmax(ym, yp), tmax(zm, zp)));
+          const T mn = tmin(tmin(tmin(nmn[q], xc), tmin(xm, xp)), tmin(tmin(ym, yp), tmin(zm, zp)));
+          const T axl = upflux(xm, xc, ucar[q]);
+          const T axr = upflux(xc, xp, ufresh[q]);
+          const T ayl = upflux(ym, xc, vA[o]);
+          const T ayr = upflux(xc, yp, vA[o + L]);
+          const T azl = upflux(zm, xc, wA[o]);
+          const T azr = upflux(xc, zp, wA[op_k]);
+          // 2*pos(f) = f + |f|, -2*neg(f) = |f| - f (both exact): the sums are
+          // the oracle's fin/fout scaled by exactly 2.
+          const T fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) + ((ayl + fabs(ayl)) + (fabs(ayr) - ayr))) +
+                         ((azl + fabs(azl)) + (fabs(azr) - azr));
+          const T fout2 = (((axr + fabs(axr)) + (fabs(axl) - axl)) + ((ayr + fabs(ayr)) + (fabs(ayl) - ayl))) +
+                          ((azr + fabs(azr)) + (fabs(azl) - azl));
           const T hc = __ldg(H1 + gj + k);
-          const T di = fin + Eps<T>::value, dou = fout + Eps<T>::value;
+          const T di = T(0.5) * fin2 + Eps<T>::value, dou = T(0.5) * fout2 + Eps<T>::value;
           T bu, bd;
           if constexpr (sizeof(T) == 8) {
             const T rr2 = rcp(di * dou);
-            bu = ((mxq[q] - xc) * hc) * dou * rr2;
-            bd = ((xc - mnq[q]) * hc) * di * rr2;
+            bu = ((mx - xc) * hc) * dou * rr2;
+            bd = ((xc - mn) * hc) * di * rr2;
           } else {
-            bu = qdiv((mxq[q] - xc) * hc, di);
-            bd = qdiv((xc - mnq[q]) * hc, dou);
+            bu = qdiv((mx - xc) * hc, di);
+            bd = qdiv((xc - mn) * hc, dou);
           }
-          bun[q] = bu;
-          bdn[q] = bd;
-          s_bu[o] = bu;
-          s_bd[o] = bd;
+          buA[o] = bu;
+          bdA[o] = bd;
         }
       }
       __syncthreads();
@@ -328,20 +362,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         for (int q = 0; q < Q; ++q) {
           IMB_CELL(q)
           if (r >= 2 && r < RR - 1)
-            vA[o] = limit(vA[o], s_bd[o - L], s_bu[o], s_bu[o - L], s_bd[o]);
+            vA[o] = limit_sel(vA[o], bdA[o - L], buA[o], buA[o - L], bdA[o]);
           if (r < 2 || r >= RR - 2) continue;
-          wA[o] = limit(wA[o], s_bd[om_k], s_bu[o], s_bu[om_k], s_bd[o]);
-          const T ul = limit(ucar[q], bdc[q], bun[q], buc[q], bdn[q]);
-          const T fxr = flux(s0[o], s1[o], ul);
+          wA[o] = limit_sel(wA[o], bdA[om_k], buA[o], buA[om_k], bdA[o]);
+          const T ul = limit_sel(ucar[q], bdB[o], buA[o], buB[o], bdA[o]);
+          const T xc = s0[o];
+          const T fxr = upflux(xc, s1[o], ul);
           if (emit) {
-            const T xc = s0[o];
-            const T fyl = flux(s0[o - L], xc, vB[o]);
-            const T fyr = flux(xc, s0[o + L], vB[o + L]);
-            const T fzl = flux(s0[om_k], xc, wB[o]);
-            const T fzr = flux(xc, s0[op_k], wB[op_k]);
+            const T fyl = upflux(s0[o - L], xc, vB[o]);
+            const T fyr = upflux(xc, s0[o + L], vB[o + L]);
+            const T fzl = upflux(s0[om_k], xc, wB[o]);
+            const T fzr = upflux(xc, s0[op_k], wB[op_k]);
             const T div = ((fxr - fxc[q]) + (fyr - fyl)) + (fzr - fzl);
             const int j = j0 + r - 2;
-            if (j < m) O[gj + k] = xc - div / __ldg(H0 + gj + k);
+            if (j < m) O[gj + k] = xc - qdiv(div, __ldg(H0 + gj + k));
           }
           fxc[q] = fxr;
         }
@@ -349,14 +383,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         ucar[q] = ufresh[q];
-        buc[q] = bun[q];
-        bdc[q] = bdn[q];
+        nmx[q] = nmx_new[q];
+        nmn[q] = nmn_new[q];
       }
       __syncthreads();
     } else {
       // Plain IORD=2: pseudo-velocities of plane t, then the final update.
-      stage_pseudo(t, false, ufresh, s_v, s_w, nullptr, nullptr);
+      stage_pseudo(t, false, ufresh, s_v, s_w);
       __syncthreads();
+      const T* sm1 = s_x1 + slot3(t - 1) * PL;
       const T* s0 = s_x1 + slot3(t) * PL;
       const T* s1 = s_x1 + slot3(t + 1) * PL;
       const T* H0 = a.h + pl(t);
@@ -366,20 +401,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         IMB_CELL(q)
         if (r < 1 || r >= RR - 1) continue;
         const T xc = s0[o];
-        const T fxl = flux(s_x1[slot3(t - 1) * PL + o], xc, ucar[q]);
-        const T fxr = flux(xc, s1[o], ufresh[q]);
-        const T fyl = flux(s0[o - L], xc, s_v[o]);
-        const T fyr = flux(xc, s0[o + L], s_v[o + L]);
-        const T fzl = flux(s0[om_k], xc, s_w[o]);
-        const T fzr = flux(xc, s0[op_k], s_w[op_k]);
+        const T fxl = upflux(sm1[o], xc, ucar[q]);
+        const T fxr = upflux(xc, s1[o], ufresh[q]);
+        const T fyl = upflux(s0[o - L], xc, s_v[o]);
+        const T fyr = upflux(xc, s0[o + L], s_v[o + L]);
+        const T fzl = upflux(s0[om_k], xc, s_w[o]);
+        const T fzr = upflux(xc, s0[op_k], s_w[op_k]);
         const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
         const int j = j0 + r - 1;
-        if (j < m) O[gj + k] = xc - div / __ldg(H0 + gj + k);
+        if (j < m) O[gj + k] = xc - qdiv(div, __ldg(H0 + gj + k));
         ucar[q] = ufresh[q];
       }
       __syncthreads();
     }
   }
+#undef IMB_CELL
 }
 
 struct Plan {
@@ -404,16 +440,16 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   return best;
 }
 
-template <class T, int L, int RW, int NW, bool NONOS>
+template <class T, int L, int RR, int NT, bool NONOS>
 int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
                T* out, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RW, NW, NONOS>;
+  using C = Cfg<T, L, RR, NT, NONOS>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
-    cudaFuncSetAttribute(k_fused<T, L, RW, NW, NONOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fused<T, L, RR, NT, NONOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RW, NW, NONOS>, C::NT,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RR, NT, NONOS>, C::NT,
                                                   C::SMEM);
     if (per_sm < 1) per_sm = 1;
     configured = true;
@@ -421,17 +457,29 @@ int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T
   const Plan p = plan_grid(fs.m, C::TJ, fs.o1 - fs.o0, per_sm * num_sms, NONOS ? 4 : 2);
   Args<T> a{x, u, v, w, h, out, static_cast<int>(fs.m), static_cast<int>(fs.R), p.ntj, p.nseg,
             static_cast<int>(fs.o0), static_cast<int>(fs.o1), fs.m * fs.l};
-  k_fused<T, L, RW, NW, NONOS><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
+  k_fused<T, L, RR, NT, NONOS><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
   return 1;
 }
 
 template <class T, bool NONOS>
 int dispatch_l(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
                T* out, int num_sms, cudaStream_t st) {
+  static const int nt = [] {
+    const char* e = std::getenv("IMB_FUSED_NT");
+    return e ? std::atoi(e) : 1024;
+  }();
+  if (nt == 512) {
+    switch (fs.l) {
+      case 128: return launch_cfg<T, 128, 16, 512, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+      case 64: return launch_cfg<T, 64, 32, 512, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+      case 32: return launch_cfg<T, 32, 64, 512, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+      default: return 0;
+    }
+  }
   switch (fs.l) {
-    case 128: return launch_cfg<T, 128, 1, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-    case 64: return launch_cfg<T, 64, 2, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-    case 32: return launch_cfg<T, 32, 4, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 128: return launch_cfg<T, 128, 16, 1024, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 64: return launch_cfg<T, 64, 32, 1024, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 32: return launch_cfg<T, 32, 64, 1024, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
     default: return 0;
   }
 }

@@ -120,8 +120,8 @@ __device__ __forceinline__ void ext7(const Span& s, const T* __restrict__ x, con
   lo = v[0];
 #pragma unroll
   for (int q = 1; q < 7; ++q) {
-    hi = fmax(hi, v[q]);
-    lo = fmin(lo, v[q]);
+    hi = tmax(hi, v[q]);
+    lo = tmin(lo, v[q]);
   }
 }
 
@@ -138,11 +138,11 @@ __global__ void __launch_bounds__(256) k_bounds(Span s, const T* __restrict__ x,
   if (first) {
     T h2, l2;
     ext7(s, xn, c, h2, l2);
-    hi = fmax(hi, h2);
-    lo = fmin(lo, l2);
+    hi = tmax(hi, h2);
+    lo = tmin(lo, l2);
   } else {
-    hi = fmax(hi, mx[o]);
-    lo = fmin(lo, mn[o]);
+    hi = tmax(hi, mx[o]);
+    lo = tmin(lo, mn[o]);
   }
   mx[o] = hi;
   mn[o] = lo;
