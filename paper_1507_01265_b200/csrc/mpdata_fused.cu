@@ -4,21 +4,23 @@
 // fluxes) lives in shared memory or registers.
 //
 // Geometry (B200-first):
-//  * k (contiguous, l <= 128) is covered completely by each warp's lanes
-//    (k = lane + 32*kk), periodic in-register wrap -> no k halo at all.
-//  * Each block owns a j-tile of TJ output rows plus a 2-row (limiter) or
-//    1-row (plain) recomputed halo on either side: RR = NW*RW region rows,
-//    one or more rows per warp, fixed for every stage.
+//  * A warp owns whole rows: each lane holds KPT = l/32 CONSECUTIVE k values
+//    of a row (l in {32, 64, 128}), so every global/shared access is a
+//    16/32-byte vector per lane and a warp moves a whole contiguous row; the
+//    k +- 1 neighbours are in-register or one warp shuffle away, with the
+//    periodic k wrap closing inside the warp (no k halo, no k-neighbour loads).
+//  * A block owns a j-tile of TJ output rows plus a recomputed halo of 2 rows
+//    (limiter) or 1 row (plain) on each side: RR = NW*RW region rows.
 //  * The block streams along i (the slab axis) over a segment of planes. The
-//    stages run with a lag of one plane each, so along i nothing is
-//    recomputed except a 2-plane warm-up per segment: smem keeps 3 planes of
-//    psi^(1), 2 of the y/z pseudo-velocities and 1 of each beta; every
-//    same-column dependency along i (x-face velocity, beta of the previous
-//    plane, the x-flux shared by two consecutive outputs) is a register
-//    carry.
+//    stages run one plane apart, so along i nothing is recomputed except a
+//    two-plane warm-up per segment. Shared memory holds 3 planes of psi^(1),
+//    2 of the y/z pseudo-velocities and 2 of each beta; same-column
+//    dependencies along i (x-face velocity, x-flux, the psi^n star extrema)
+//    are register carries.
 //  * Divisions: fp64 folds the four divisions of a pseudo-velocity into one
-//    reciprocal of hb*dA*dB*dC and the two beta divisions into one; fp32
-//    uses the fast reciprocal. Both stay inside the parity tolerance.
+//    reciprocal of hb*dA*dB*dC and the two beta divisions into one, with a
+//    MUFU seed + 2 Newton steps; fp32 uses MUFU.RCP. Both stay inside the
+//    parity tolerance (1e-12 / 1e-5).
 // The per-cell arithmetic follows SURVEY.md Appendix A (see mpdata_math.cuh).
 #include <cuda_runtime.h>
 
@@ -33,14 +35,15 @@ namespace imb::dev {
 
 namespace {
 
-template <class T, int L, int RR_, int NT_, bool NONOS>
+constexpr unsigned kFull = 0xffffffffu;
+
+template <class T, int L, int RW, int NW, bool NONOS>
 struct Cfg {
-  static constexpr int RR = RR_;                  // region rows
-  static constexpr int Q = RR * L / NT_;          // cells per thread
-  static_assert(Q * NT_ == RR * L && NT_ % L == 0, "threads must tile whole rows");
+  static constexpr int KPT = L / 32;              // consecutive k per lane
+  static constexpr int RR = NW * RW;              // region rows
   static constexpr int HALO = NONOS ? 2 : 1;      // recomputed rows on each side
   static constexpr int TJ = RR - 2 * HALO;        // output rows per tile
-  static constexpr int NT = NT_;
+  static constexpr int NT = NW * 32;
   static constexpr int PLANE = RR * L;            // cells of one smem plane
   static constexpr int NSLOT = NONOS ? 11 : 5;
   static constexpr std::size_t SMEM = sizeof(T) * PLANE * NSLOT;
@@ -61,6 +64,97 @@ struct Args {
   int o0, o1;       // output plane range (interior coordinates)
   long long plane;  // m * l
 };
+
+// ---- per-lane vectors of K consecutive k values ---------------------------
+template <class T, int K>
+struct Vec {
+  T e[K];
+};
+
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> vload(const T* p) {  // global, read-only path
+  Vec<T, K> r;
+  if constexpr (sizeof(T) == 8 && K == 4) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
+  } else if constexpr (sizeof(T) == 8 && K == 2) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    r.e[0] = a.x; r.e[1] = a.y;
+  } else if constexpr (sizeof(T) == 4 && K == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = a.z; r.e[3] = a.w;
+  } else if constexpr (sizeof(T) == 4 && K == 2) {
+    const float2 a = __ldg(reinterpret_cast<const float2*>(p));
+    r.e[0] = a.x; r.e[1] = a.y;
+  } else {
+    r.e[0] = __ldg(p);
+  }
+  return r;
+}
+
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> sload(const T* p) {  // shared
+  Vec<T, K> r;
+  if constexpr (sizeof(T) == 8 && K == 4) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    const double2 b = reinterpret_cast<const double2*>(p)[1];
+    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
+  } else if constexpr (sizeof(T) == 8 && K == 2) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    r.e[0] = a.x; r.e[1] = a.y;
+  } else if constexpr (sizeof(T) == 4 && K == 4) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0];
+    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = a.z; r.e[3] = a.w;
+  } else if constexpr (sizeof(T) == 4 && K == 2) {
+    const float2 a = reinterpret_cast<const float2*>(p)[0];
+    r.e[0] = a.x; r.e[1] = a.y;
+  } else {
+    r.e[0] = p[0];
+  }
+  return r;
+}
+
+template <class T, int K>
+__device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or global
+  if constexpr (sizeof(T) == 8 && K == 4) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v.e[2], v.e[3]);
+  } else if constexpr (sizeof(T) == 8 && K == 2) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
+  } else if constexpr (sizeof(T) == 4 && K == 4) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v.e[0], v.e[1], v.e[2], v.e[3]);
+  } else if constexpr (sizeof(T) == 4 && K == 2) {
+    reinterpret_cast<float2*>(p)[0] = make_float2(v.e[0], v.e[1]);
+  } else {
+    p[0] = v.e[0];
+  }
+}
+
+// Value at k-1 / k+1 (periodic in k: the warp holds the whole row).
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, int lane) {
+  Vec<T, K> r;
+  r.e[0] = __shfl_sync(kFull, a.e[K - 1], (lane + 31) & 31);
+#pragma unroll
+  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
+  return r;
+}
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, int lane) {
+  Vec<T, K> r;
+  r.e[K - 1] = __shfl_sync(kFull, a.e[0], (lane + 1) & 31);
+#pragma unroll
+  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
+  return r;
+}
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> vabs(const Vec<T, K>& a) {
+  Vec<T, K> r;
+#pragma unroll
+  for (int e = 0; e < K; ++e) r.e[e] = fabs(a.e[e]);
+  return r;
+}
 
 // Reciprocals without the IEEE-division slow path: fp64 = MUFU.RCP64H seed +
 // two Newton steps (error ~2^-80 before the final rounding, i.e. within an
@@ -87,7 +181,7 @@ template <class T>
 __device__ __forceinline__ T upflux(T a, T b, T c) {
   return c * (c > T(0) ? a : b);
 }
-// Limited velocity: vel * min(1, bdL, buR) for outflow to the right, else
+// Limited velocity: vel * min(1, bdL, buR) for vel > 0, else
 // vel * min(1, buL, bdR) — equal to dev::limit exactly.
 template <class T>
 __device__ __forceinline__ T limit_sel(T vel, T bdL, T buR, T buL, T bdR) {
@@ -124,11 +218,11 @@ __device__ __forceinline__ T pseudo_face(T Un, T hL, T hR, T aR, T aL, T bp, T b
   }
 }
 
-template <class T, int L, int RR_, int NT, bool NONOS>
-__global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RR_, NT, NONOS>;
-  constexpr int Q = C::Q, RR = C::RR, PL = C::PLANE;
-  constexpr int RSTEP = NT / L;  // rows between a thread's consecutive cells
+template <class T, int L, int RW, int NW, bool NONOS>
+__global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
+  using C = Cfg<T, L, RW, NW, NONOS>;
+  constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE;
+  using V = Vec<T, K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   T* s_x1 = sm;                          // 3 slots of psi^(1), by plane mod 3
@@ -145,31 +239,26 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
   if (ib >= ie) return;
   const int j0 = tile * C::TJ;
   const int m = a.m;
-  // Thread -> cells: cell q is (row r0 + q*RSTEP, column k); a warp covers 32
-  // consecutive k of one row, so every row test below is warp-uniform.
-  const int r0 = threadIdx.x / L, kc = threadIdx.x % L;
-  int gjr[Q], gjmr[Q], gjpr[Q];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kl = lane * K;  // first k of this lane
+
+  // Rows of this warp: region row r = warp*RW + rr; global offsets of the
+  // row (j wraps periodically) and of its j-1 / j+1 neighbours.
+  int gj[RW], gjm[RW], gjp[RW];
 #pragma unroll
-  for (int rr = 0; rr < Q; ++rr) {
-    int j = j0 - C::HALO + r0 + rr * RSTEP;
+  for (int rr = 0; rr < RW; ++rr) {
+    int j = j0 - C::HALO + warp * RW + rr;
     j = ((j % m) + m) % m;
-    gjr[rr] = j * L;
-    gjmr[rr] = (j == 0 ? m - 1 : j - 1) * L;
-    gjpr[rr] = (j == m - 1 ? 0 : j + 1) * L;
+    gj[rr] = j * L + kl;
+    gjm[rr] = (j == 0 ? m - 1 : j - 1) * L + kl;
+    gjp[rr] = (j == m - 1 ? 0 : j + 1) * L + kl;
   }
-#define IMB_CELL(q)                                                   \
-  const int rr_ = (q);                                                \
-  const int r = r0 + rr_ * RSTEP;                                     \
-  const int k = kc;                                                   \
-  const int km = k == 0 ? L - 1 : k - 1, kp = k == L - 1 ? 0 : k + 1; \
-  const int o = r * L + k, om_k = r * L + km, op_k = r * L + kp;      \
-  const int gj = gjr[rr_], gjm = gjmr[rr_], gjp = gjpr[rr_];          \
-  (void)om_k; (void)op_k; (void)gjm; (void)gjp; (void)km; (void)kp;
   auto slot3 = [](int p) { return (p + 6) % 3; };  // p >= -3
   auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
+  auto srow = [&](int r) { return r * L + kl; };  // smem offset of a row vector
 
-  // ψn star extrema of the newest donor plane (NONOS), carried one plane.
-  T nmx_new[Q], nmn_new[Q], nmx[Q], nmn[Q];
+  V nmx_new[RW], nmn_new[RW], nmx[RW], nmn[RW];  // psi^n star extrema (NONOS)
+
   // P1: psi^(1) at plane p (donor cell) for all region rows.
   auto stage_donor = [&](int p) {
     const T* X = a.x + pl(p);
@@ -177,36 +266,48 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
     const T* Xp = a.x + pl(p + 1);
     const T* U = a.u + pl(p);
     const T* Up = a.u + pl(p + 1);
-    const T* V = a.v + pl(p);
+    const T* Vv = a.v + pl(p);
     const T* W = a.w + pl(p);
     const T* H = a.h + pl(p);
     T* dst = s_x1 + slot3(p) * PL;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      IMB_CELL(q)
-      const int c = gj + k;
-      const T xc = __ldg(X + c);
-      const T xm = __ldg(Xm + c), xp = __ldg(Xp + c);
-      const T ym = __ldg(X + gjm + k), yp = __ldg(X + gjp + k);
-      const T zm = __ldg(X + gj + km), zp = __ldg(X + gj + kp);
-      const T fxl = upflux(xm, xc, __ldg(U + c));
-      const T fxr = upflux(xc, xp, __ldg(Up + c));
-      const T fyl = upflux(ym, xc, __ldg(V + c));
-      const T fyr = upflux(xc, yp, __ldg(V + gjp + k));
-      const T fzl = upflux(zm, xc, __ldg(W + c));
-      const T fzr = upflux(xc, zp, __ldg(W + gj + kp));
-      const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-      dst[o] = xc - qdiv(div, __ldg(H + c));
-      if constexpr (NONOS) {
-        nmx_new[q] = tmax(tmax(tmax(xc, xm), tmax(xp, ym)), tmax(tmax(yp, zm), zp));
-        nmn_new[q] = tmin(tmin(tmin(xc, xm), tmin(xp, ym)), tmin(tmin(yp, zm), zp));
+    for (int rr = 0; rr < RW; ++rr) {
+      const int r = warp * RW + rr;
+      const V xc = vload<T, K>(X + gj[rr]);
+      const V xm = vload<T, K>(Xm + gj[rr]), xp = vload<T, K>(Xp + gj[rr]);
+      const V ym = vload<T, K>(X + gjm[rr]), yp = vload<T, K>(X + gjp[rr]);
+      const V zm = kminus(xc, lane), zp = kplus(xc, lane);
+      const V uc = vload<T, K>(U + gj[rr]), up = vload<T, K>(Up + gj[rr]);
+      const V vc = vload<T, K>(Vv + gj[rr]), vp = vload<T, K>(Vv + gjp[rr]);
+      const V wc = vload<T, K>(W + gj[rr]);
+      const V wp = kplus(wc, lane);
+      const V hc = vload<T, K>(H + gj[rr]);
+      V res;
+#pragma unroll
+      for (int e = 0; e < K; ++e) {
+        const T c = xc.e[e];
+        const T fxl = upflux(xm.e[e], c, uc.e[e]);
+        const T fxr = upflux(c, xp.e[e], up.e[e]);
+        const T fyl = upflux(ym.e[e], c, vc.e[e]);
+        const T fyr = upflux(c, yp.e[e], vp.e[e]);
+        const T fzl = upflux(zm.e[e], c, wc.e[e]);
+        const T fzr = upflux(c, zp.e[e], wp.e[e]);
+        const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
+        res.e[e] = c - qdiv(div, hc.e[e]);
+        if constexpr (NONOS) {
+          nmx_new[rr].e[e] = tmax(tmax(tmax(c, xm.e[e]), tmax(xp.e[e], ym.e[e])),
+                                  tmax(tmax(yp.e[e], zm.e[e]), zp.e[e]));
+          nmn_new[rr].e[e] = tmin(tmin(tmin(c, xm.e[e]), tmin(xp.e[e], ym.e[e])),
+                                  tmin(tmin(yp.e[e], zm.e[e]), zp.e[e]));
+        }
       }
+      vstore(dst + srow(r), res);
     }
   };
 
   // P2: pseudo-velocities around base plane pb: x-face pb+1 (into ut), y and
   // z faces of plane pb (into smem).
-  auto stage_pseudo = [&](int pb, bool only_u, T* ut, T* vdst, T* wdst) {
+  auto stage_pseudo = [&](int pb, bool only_u, V* ut, T* vdst, T* wdst) {
     const T* s0 = s_x1 + slot3(pb - 1) * PL;
     const T* s1 = s_x1 + slot3(pb) * PL;
     const T* s2 = s_x1 + slot3(pb + 1) * PL;
@@ -219,63 +320,91 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
     const T* H1 = a.h + pl(pb);
     const T* H2 = a.h + pl(pb + 1);
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      IMB_CELL(q)
-      const int c = gj + k;
-      const bool row_u = r >= 1 && r < RR - 1;  // x/z faces
-      const bool row_v = r >= 1;                // y faces
-      const T a1c = fabs(s1[o]);
-      const T u2c = __ldg(U2 + c), h1c = __ldg(H1 + c);
+    for (int rr = 0; rr < RW; ++rr) {
+      const int r = warp * RW + rr;
+      if (r < 1) continue;  // warp-uniform
+      const bool row_u = r < RR - 1;  // x/z faces (y faces: every r >= 1)
+      const V a1 = vabs(sload<T, K>(s1 + srow(r)));
+      const V a1m = vabs(sload<T, K>(s1 + srow(r - 1)));
+      const V u2c = vload<T, K>(U2 + gj[rr]);
+      const V h1c = vload<T, K>(H1 + gj[rr]);
+      const V a1km = kminus(a1, lane);
       if (row_u) {  // x-face between planes pb and pb+1 of this column
-        const T a2c = fabs(s2[o]);
-        const T bp = fabs(s1[o + L]) + fabs(s2[o + L]);
-        const T bm = fabs(s1[o - L]) + fabs(s2[o - L]);
-        const T cp = fabs(s1[op_k]) + fabs(s2[op_k]);
-        const T cm = fabs(s1[om_k]) + fabs(s2[om_k]);
-        const int cjp = gjp + k, ckp = gj + kp;
-        const T Vs = (__ldg(V1 + c) + __ldg(V2 + c)) + (__ldg(V1 + cjp) + __ldg(V2 + cjp));
-        const T Ws = (__ldg(W1 + c) + __ldg(W2 + c)) + (__ldg(W1 + ckp) + __ldg(W2 + ckp));
-        ut[q] = pseudo_face<T>(u2c, h1c, __ldg(H2 + c), a2c, a1c, bp, bm, Vs, cp, cm, Ws);
+        const V a2 = vabs(sload<T, K>(s2 + srow(r)));
+        const V a1p = vabs(sload<T, K>(s1 + srow(r + 1)));
+        const V a2p = vabs(sload<T, K>(s2 + srow(r + 1)));
+        const V a2m = vabs(sload<T, K>(s2 + srow(r - 1)));
+        const V a1kp = kplus(a1, lane), a2kp = kplus(a2, lane), a2km = kminus(a2, lane);
+        const V v1 = vload<T, K>(V1 + gj[rr]), v2 = vload<T, K>(V2 + gj[rr]);
+        const V v1p = vload<T, K>(V1 + gjp[rr]), v2p = vload<T, K>(V2 + gjp[rr]);
+        const V w1 = vload<T, K>(W1 + gj[rr]), w2 = vload<T, K>(W2 + gj[rr]);
+        const V w1p = kplus(w1, lane), w2p = kplus(w2, lane);
+        const V h2 = vload<T, K>(H2 + gj[rr]);
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+          const T Vs = (v1.e[e] + v2.e[e]) + (v1p.e[e] + v2p.e[e]);
+          const T Ws = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
+          ut[rr].e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e],
+                                       a1p.e[e] + a2p.e[e], a1m.e[e] + a2m.e[e], Vs,
+                                       a1kp.e[e] + a2kp.e[e], a1km.e[e] + a2km.e[e], Ws);
+        }
       }
       if (only_u) continue;
-      const T u1c = __ldg(U1 + c);
-      if (row_v) {  // y-face between rows r-1 and r of plane pb
-        const int om = o - L;
-        const int cjm = gjm + k;
-        const T aL = fabs(s1[om]);
-        const T bp = fabs(s2[om]) + fabs(s2[o]);
-        const T bm = fabs(s0[om]) + fabs(s0[o]);
-        const T cp = fabs(s1[op_k - L]) + fabs(s1[op_k]);
-        const T cm = fabs(s1[om_k - L]) + fabs(s1[om_k]);
-        const T Us = (__ldg(U1 + cjm) + u1c) + (__ldg(U2 + cjm) + u2c);
-        const int cjmkp = gjm + kp, ckp = gj + kp;
-        const T Ws = (__ldg(W1 + cjm) + __ldg(W1 + c)) + (__ldg(W1 + cjmkp) + __ldg(W1 + ckp));
-        vdst[o] = pseudo_face<T>(__ldg(V1 + c), __ldg(H1 + cjm), h1c, a1c, aL, bp, bm, Us, cp, cm,
-                                 Ws);
+      const V a0 = vabs(sload<T, K>(s0 + srow(r)));
+      const V a2 = vabs(sload<T, K>(s2 + srow(r)));
+      const V u1c = vload<T, K>(U1 + gj[rr]);
+      const V w1 = vload<T, K>(W1 + gj[rr]);
+      {  // y-face between rows r-1 and r of plane pb
+        const V a0m = vabs(sload<T, K>(s0 + srow(r - 1)));
+        const V a2m = vabs(sload<T, K>(s2 + srow(r - 1)));
+        const V a1mkp = kplus(a1m, lane), a1mkm = kminus(a1m, lane), a1kp = kplus(a1, lane);
+        const V u1m = vload<T, K>(U1 + gjm[rr]), u2m = vload<T, K>(U2 + gjm[rr]);
+        const V w1m = vload<T, K>(W1 + gjm[rr]);
+        const V w1mkp = kplus(w1m, lane), w1kp = kplus(w1, lane);
+        const V v1 = vload<T, K>(V1 + gj[rr]);
+        const V h1m = vload<T, K>(H1 + gjm[rr]);
+        V res;
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+          const T Us = (u1m.e[e] + u1c.e[e]) + (u2m.e[e] + u2c.e[e]);
+          const T Ws = (w1m.e[e] + w1.e[e]) + (w1mkp.e[e] + w1kp.e[e]);
+          res.e[e] = pseudo_face<T>(v1.e[e], h1m.e[e], h1c.e[e], a1.e[e], a1m.e[e],
+                                    a2m.e[e] + a2.e[e], a0m.e[e] + a0.e[e], Us,
+                                    a1mkp.e[e] + a1kp.e[e], a1mkm.e[e] + a1km.e[e], Ws);
+        }
+        vstore(vdst + srow(r), res);
       }
       if (row_u) {  // z-face between k-1 and k
-        const int ckm = gj + km;
-        const T aL = fabs(s1[om_k]);
-        const T bp = fabs(s2[om_k]) + fabs(s2[o]);
-        const T bm = fabs(s0[om_k]) + fabs(s0[o]);
-        const T cp = fabs(s1[om_k + L]) + fabs(s1[o + L]);
-        const T cm = fabs(s1[om_k - L]) + fabs(s1[o - L]);
-        const T Us = (__ldg(U1 + ckm) + u1c) + (__ldg(U2 + ckm) + u2c);
-        const int cjpkm = gjp + km, cjp = gjp + k;
-        const T Vs = (__ldg(V1 + ckm) + __ldg(V1 + c)) + (__ldg(V1 + cjpkm) + __ldg(V1 + cjp));
-        wdst[o] = pseudo_face<T>(__ldg(W1 + c), __ldg(H1 + ckm), h1c, a1c, aL, bp, bm, Us, cp, cm,
-                                 Vs);
+        const V a1p = vabs(sload<T, K>(s1 + srow(r + 1)));
+        const V a1pkm = kminus(a1p, lane), a1mkm = kminus(a1m, lane);
+        const V a2km = kminus(a2, lane), a0km = kminus(a0, lane);
+        const V u2km = kminus(u2c, lane), u1km = kminus(u1c, lane);
+        const V v1 = vload<T, K>(V1 + gj[rr]), v1p = vload<T, K>(V1 + gjp[rr]);
+        const V v1km = kminus(v1, lane), v1pkm = kminus(v1p, lane);
+        const V h1km = kminus(h1c, lane);
+        V res;
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+          const T Us = (u1km.e[e] + u1c.e[e]) + (u2km.e[e] + u2c.e[e]);
+          const T Vs = (v1km.e[e] + v1.e[e]) + (v1pkm.e[e] + v1p.e[e]);
+          res.e[e] = pseudo_face<T>(w1.e[e], h1km.e[e], h1c.e[e], a1.e[e], a1km.e[e],
+                                    a2km.e[e] + a2.e[e], a0km.e[e] + a0.e[e], Us,
+                                    a1pkm.e[e] + a1p.e[e], a1mkm.e[e] + a1m.e[e], Vs);
+        }
+        vstore(wdst + srow(r), res);
       }
     }
   };
 
   // ---- register carries along i (same (j,k) column) -------------------------
-  T ucar[Q], ufresh[Q], fxc[Q];
+  V ucar[RW], ufresh[RW], fxc[RW];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    ucar[q] = ufresh[q] = fxc[q] = T(0);
-    nmx[q] = nmn[q] = nmx_new[q] = nmn_new[q] = T(0);
-  }
+  for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      ucar[rr].e[e] = ufresh[rr].e[e] = fxc[rr].e[e] = T(0);
+      nmx[rr].e[e] = nmn[rr].e[e] = nmx_new[rr].e[e] = nmn_new[rr].e[e] = T(0);
+    }
 
   const int lag = NONOS ? 2 : 1;  // psi^(1) planes ahead of the output plane
   // warm-up: psi^(1) on the first two planes of the window, then the x-face
@@ -284,9 +413,9 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
   stage_donor(ib - lag + 1);
   if constexpr (NONOS) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      nmx[q] = nmx_new[q];
-      nmn[q] = nmn_new[q];
+    for (int rr = 0; rr < RW; ++rr) {
+      nmx[rr] = nmx_new[rr];
+      nmn[rr] = nmn_new[rr];
     }
   }
   __syncthreads();
@@ -316,39 +445,51 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
         const T* s2 = s_x1 + slot3(t + 2) * PL;
         const T* H1 = a.h + pl(p1);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          IMB_CELL(q)
+        for (int rr = 0; rr < RW; ++rr) {
+          const int r = warp * RW + rr;
           if (r < 1 || r >= RR - 1) continue;
-          const T xc = s1[o];
-          const T xm = s0[o], xp = s2[o], ym = s1[o - L], yp = s1[o + L];
-          const T zm = s1[om_k], zp = s1[op_k];
-          const T mx = tmax(tmax(tmax(nmx[q], xc), tmax(xm, xp)), tmax(tmax(ym, yp), tmax(zm, zp)));
-          const T mn = tmin(tmin(tmin(nmn[q], xc), tmin(xm, xp)), tmin(tmin(ym, yp), tmin(zm, zp)));
-          const T axl = upflux(xm, xc, ucar[q]);
-          const T axr = upflux(xc, xp, ufresh[q]);
-          const T ayl = upflux(ym, xc, vA[o]);
-          const T ayr = upflux(xc, yp, vA[o + L]);
-          const T azl = upflux(zm, xc, wA[o]);
-          const T azr = upflux(xc, zp, wA[op_k]);
-          // 2*pos(f) = f + |f|, -2*neg(f) = |f| - f (both exact): the sums are
-          // the oracle's fin/fout scaled by exactly 2.
-          const T fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) + ((ayl + fabs(ayl)) + (fabs(ayr) - ayr))) +
-                         ((azl + fabs(azl)) + (fabs(azr) - azr));
-          const T fout2 = (((axr + fabs(axr)) + (fabs(axl) - axl)) + ((ayr + fabs(ayr)) + (fabs(ayl) - ayl))) +
-                          ((azr + fabs(azr)) + (fabs(azl) - azl));
-          const T hc = __ldg(H1 + gj + k);
-          const T di = T(0.5) * fin2 + Eps<T>::value, dou = T(0.5) * fout2 + Eps<T>::value;
-          T bu, bd;
-          if constexpr (sizeof(T) == 8) {
-            const T rr2 = rcp(di * dou);
-            bu = ((mx - xc) * hc) * dou * rr2;
-            bd = ((xc - mn) * hc) * di * rr2;
-          } else {
-            bu = qdiv((mx - xc) * hc, di);
-            bd = qdiv((xc - mn) * hc, dou);
+          const V xc = sload<T, K>(s1 + srow(r));
+          const V xm = sload<T, K>(s0 + srow(r)), xp = sload<T, K>(s2 + srow(r));
+          const V ym = sload<T, K>(s1 + srow(r - 1)), yp = sload<T, K>(s1 + srow(r + 1));
+          const V zm = kminus(xc, lane), zp = kplus(xc, lane);
+          const V va = sload<T, K>(vA + srow(r)), vap = sload<T, K>(vA + srow(r + 1));
+          const V wa = sload<T, K>(wA + srow(r));
+          const V wap = kplus(wa, lane);
+          const V hc = vload<T, K>(H1 + gj[rr]);
+          V bu, bd;
+#pragma unroll
+          for (int e = 0; e < K; ++e) {
+            const T c = xc.e[e];
+            const T mx = tmax(tmax(tmax(nmx[rr].e[e], c), tmax(xm.e[e], xp.e[e])),
+                              tmax(tmax(ym.e[e], yp.e[e]), tmax(zm.e[e], zp.e[e])));
+            const T mn = tmin(tmin(tmin(nmn[rr].e[e], c), tmin(xm.e[e], xp.e[e])),
+                              tmin(tmin(ym.e[e], yp.e[e]), tmin(zm.e[e], zp.e[e])));
+            const T axl = upflux(xm.e[e], c, ucar[rr].e[e]);
+            const T axr = upflux(c, xp.e[e], ufresh[rr].e[e]);
+            const T ayl = upflux(ym.e[e], c, va.e[e]);
+            const T ayr = upflux(c, yp.e[e], vap.e[e]);
+            const T azl = upflux(zm.e[e], c, wa.e[e]);
+            const T azr = upflux(c, zp.e[e], wap.e[e]);
+            // 2*pos(f) = f + |f| and -2*neg(f) = |f| - f are exact, so these
+            // are the oracle's inflow/outflow sums scaled by exactly 2.
+            const T fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) +
+                            ((ayl + fabs(ayl)) + (fabs(ayr) - ayr))) +
+                           ((azl + fabs(azl)) + (fabs(azr) - azr));
+            const T fout2 = (((axr + fabs(axr)) + (fabs(axl) - axl)) +
+                             ((ayr + fabs(ayr)) + (fabs(ayl) - ayl))) +
+                            ((azr + fabs(azr)) + (fabs(azl) - azl));
+            const T di = T(0.5) * fin2 + Eps<T>::value, dou = T(0.5) * fout2 + Eps<T>::value;
+            if constexpr (sizeof(T) == 8) {
+              const T rr2 = rcp(di * dou);
+              bu.e[e] = ((mx - c) * hc.e[e]) * dou * rr2;
+              bd.e[e] = ((c - mn) * hc.e[e]) * di * rr2;
+            } else {
+              bu.e[e] = qdiv((mx - c) * hc.e[e], di);
+              bd.e[e] = qdiv((c - mn) * hc.e[e], dou);
+            }
           }
-          buA[o] = bu;
-          bdA[o] = bd;
+          vstore(buA + srow(r), bu);
+          vstore(bdA + srow(r), bd);
         }
       }
       __syncthreads();
@@ -359,32 +500,62 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
         const T* H0 = a.h + pl(t);
         T* O = a.out + pl(t);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          IMB_CELL(q)
-          if (r >= 2 && r < RR - 1)
-            vA[o] = limit_sel(vA[o], bdA[o - L], buA[o], buA[o - L], bdA[o]);
-          if (r < 2 || r >= RR - 2) continue;
-          wA[o] = limit_sel(wA[o], bdA[om_k], buA[o], buA[om_k], bdA[o]);
-          const T ul = limit_sel(ucar[q], bdB[o], buA[o], buB[o], bdA[o]);
-          const T xc = s0[o];
-          const T fxr = upflux(xc, s1[o], ul);
-          if (emit) {
-            const T fyl = upflux(s0[o - L], xc, vB[o]);
-            const T fyr = upflux(xc, s0[o + L], vB[o + L]);
-            const T fzl = upflux(s0[om_k], xc, wB[o]);
-            const T fzr = upflux(xc, s0[op_k], wB[op_k]);
-            const T div = ((fxr - fxc[q]) + (fyr - fyl)) + (fzr - fzl);
-            const int j = j0 + r - 2;
-            if (j < m) O[gj + k] = xc - qdiv(div, __ldg(H0 + gj + k));
+        for (int rr = 0; rr < RW; ++rr) {
+          const int r = warp * RW + rr;
+          if (r < 2 || r >= RR - 1) continue;
+          const V bu = sload<T, K>(buA + srow(r)), bd = sload<T, K>(bdA + srow(r));
+          {
+            const V va = sload<T, K>(vA + srow(r));
+            const V bum = sload<T, K>(buA + srow(r - 1)), bdm = sload<T, K>(bdA + srow(r - 1));
+            V res;
+#pragma unroll
+            for (int e = 0; e < K; ++e)
+              res.e[e] = limit_sel(va.e[e], bdm.e[e], bu.e[e], bum.e[e], bd.e[e]);
+            vstore(vA + srow(r), res);
           }
-          fxc[q] = fxr;
+          if (r >= RR - 2) continue;
+          const V wa = sload<T, K>(wA + srow(r));
+          const V bukm = kminus(bu, lane), bdkm = kminus(bd, lane);
+          const V buo = sload<T, K>(buB + srow(r)), bdo = sload<T, K>(bdB + srow(r));
+          const V xc = sload<T, K>(s0 + srow(r));
+          const V x1 = sload<T, K>(s1 + srow(r));
+          V wres, fxr;
+#pragma unroll
+          for (int e = 0; e < K; ++e) {
+            wres.e[e] = limit_sel(wa.e[e], bdkm.e[e], bu.e[e], bukm.e[e], bd.e[e]);
+            const T ul = limit_sel(ucar[rr].e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
+            fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
+          }
+          vstore(wA + srow(r), wres);
+          if (emit) {
+            const V ym = sload<T, K>(s0 + srow(r - 1)), yp = sload<T, K>(s0 + srow(r + 1));
+            const V zm = kminus(xc, lane), zp = kplus(xc, lane);
+            const V vb = sload<T, K>(vB + srow(r)), vbp = sload<T, K>(vB + srow(r + 1));
+            const V wb = sload<T, K>(wB + srow(r));
+            const V wbp = kplus(wb, lane);
+            const V hc = vload<T, K>(H0 + gj[rr]);
+            V res;
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+              const T c = xc.e[e];
+              const T fyl = upflux(ym.e[e], c, vb.e[e]);
+              const T fyr = upflux(c, yp.e[e], vbp.e[e]);
+              const T fzl = upflux(zm.e[e], c, wb.e[e]);
+              const T fzr = upflux(c, zp.e[e], wbp.e[e]);
+              const T div = ((fxr.e[e] - fxc[rr].e[e]) + (fyr - fyl)) + (fzr - fzl);
+              res.e[e] = c - qdiv(div, hc.e[e]);
+            }
+            const int j = j0 + r - 2;
+            if (j < m) vstore(O + gj[rr], res);
+          }
+          fxc[rr] = fxr;
         }
       }
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        ucar[q] = ufresh[q];
-        nmx[q] = nmx_new[q];
-        nmn[q] = nmn_new[q];
+      for (int rr = 0; rr < RW; ++rr) {
+        ucar[rr] = ufresh[rr];
+        nmx[rr] = nmx_new[rr];
+        nmn[rr] = nmn_new[rr];
       }
       __syncthreads();
     } else {
@@ -397,25 +568,37 @@ __global__ void __launch_bounds__(NT, 1) k_fused(Args<T> a) {
       const T* H0 = a.h + pl(t);
       T* O = a.out + pl(t);
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        IMB_CELL(q)
+      for (int rr = 0; rr < RW; ++rr) {
+        const int r = warp * RW + rr;
         if (r < 1 || r >= RR - 1) continue;
-        const T xc = s0[o];
-        const T fxl = upflux(sm1[o], xc, ucar[q]);
-        const T fxr = upflux(xc, s1[o], ufresh[q]);
-        const T fyl = upflux(s0[o - L], xc, s_v[o]);
-        const T fyr = upflux(xc, s0[o + L], s_v[o + L]);
-        const T fzl = upflux(s0[om_k], xc, s_w[o]);
-        const T fzr = upflux(xc, s0[op_k], s_w[op_k]);
-        const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
+        const V xc = sload<T, K>(s0 + srow(r));
+        const V xm = sload<T, K>(sm1 + srow(r)), xp = sload<T, K>(s1 + srow(r));
+        const V ym = sload<T, K>(s0 + srow(r - 1)), yp = sload<T, K>(s0 + srow(r + 1));
+        const V zm = kminus(xc, lane), zp = kplus(xc, lane);
+        const V vv = sload<T, K>(s_v + srow(r)), vvp = sload<T, K>(s_v + srow(r + 1));
+        const V ww = sload<T, K>(s_w + srow(r));
+        const V wwp = kplus(ww, lane);
+        const V hc = vload<T, K>(H0 + gj[rr]);
+        V res;
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+          const T c = xc.e[e];
+          const T fxl = upflux(xm.e[e], c, ucar[rr].e[e]);
+          const T fxr = upflux(c, xp.e[e], ufresh[rr].e[e]);
+          const T fyl = upflux(ym.e[e], c, vv.e[e]);
+          const T fyr = upflux(c, yp.e[e], vvp.e[e]);
+          const T fzl = upflux(zm.e[e], c, ww.e[e]);
+          const T fzr = upflux(c, zp.e[e], wwp.e[e]);
+          const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
+          res.e[e] = c - qdiv(div, hc.e[e]);
+        }
         const int j = j0 + r - 1;
-        if (j < m) O[gj + k] = xc - qdiv(div, __ldg(H0 + gj + k));
-        ucar[q] = ufresh[q];
+        if (j < m) vstore(O + gj[rr], res);
+        ucar[rr] = ufresh[rr];
       }
       __syncthreads();
     }
   }
-#undef IMB_CELL
 }
 
 struct Plan {
@@ -440,16 +623,16 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   return best;
 }
 
-template <class T, int L, int RR, int NT, bool NONOS>
+template <class T, int L, int RW, int NW, bool NONOS>
 int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
                T* out, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RR, NT, NONOS>;
+  using C = Cfg<T, L, RW, NW, NONOS>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
-    cudaFuncSetAttribute(k_fused<T, L, RR, NT, NONOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fused<T, L, RW, NW, NONOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RR, NT, NONOS>, C::NT,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RW, NW, NONOS>, C::NT,
                                                   C::SMEM);
     if (per_sm < 1) per_sm = 1;
     configured = true;
@@ -457,29 +640,17 @@ int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T
   const Plan p = plan_grid(fs.m, C::TJ, fs.o1 - fs.o0, per_sm * num_sms, NONOS ? 4 : 2);
   Args<T> a{x, u, v, w, h, out, static_cast<int>(fs.m), static_cast<int>(fs.R), p.ntj, p.nseg,
             static_cast<int>(fs.o0), static_cast<int>(fs.o1), fs.m * fs.l};
-  k_fused<T, L, RR, NT, NONOS><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
+  k_fused<T, L, RW, NW, NONOS><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
   return 1;
 }
 
 template <class T, bool NONOS>
 int dispatch_l(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
                T* out, int num_sms, cudaStream_t st) {
-  static const int nt = [] {
-    const char* e = std::getenv("IMB_FUSED_NT");
-    return e ? std::atoi(e) : 1024;
-  }();
-  if (nt == 512) {
-    switch (fs.l) {
-      case 128: return launch_cfg<T, 128, 16, 512, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-      case 64: return launch_cfg<T, 64, 32, 512, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-      case 32: return launch_cfg<T, 32, 64, 512, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-      default: return 0;
-    }
-  }
   switch (fs.l) {
-    case 128: return launch_cfg<T, 128, 16, 1024, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-    case 64: return launch_cfg<T, 64, 32, 1024, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-    case 32: return launch_cfg<T, 32, 64, 1024, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 128: return launch_cfg<T, 128, 1, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 64: return launch_cfg<T, 64, 2, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 32: return launch_cfg<T, 32, 4, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
     default: return 0;
   }
 }

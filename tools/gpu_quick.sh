@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "fused or config or group" > gpurun_out/pytest_quick.log 2>&1
 echo "pytest=$?"; tail -3 gpurun_out/pytest_quick.log
-for nt in ${NTS:-512 1024}; do
+for nt in ${NTS:-default}; do
   echo "IMB_FUSED_NT=$nt"
   for c in c4 c2 c1; do IMB_FUSED_NT=$nt python tools/profile_step.py --config $c --warm 2 --steps 10; done
   IMB_FUSED_NT=$nt python tools/profile_step.py --config c4 --fp32 --warm 2 --steps 10
