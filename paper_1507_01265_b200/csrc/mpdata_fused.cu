@@ -37,9 +37,10 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-template <class T, int L, int RW, int NW, bool NONOS>
+template <class T, int L, int RW, int NW, int NS, bool NONOS>
 struct Cfg {
-  static constexpr int KPT = L / 32;              // consecutive k per lane
+  static constexpr int KPT = L / (32 * NS);       // consecutive k per lane and segment
+  static_assert(KPT * 32 * NS == L, "row must split into NS warp-wide segments");
   static constexpr int RR = NW * RW;              // region rows
   static constexpr int HALO = NONOS ? 2 : 1;      // recomputed rows on each side
   static constexpr int TJ = RR - 2 * HALO;        // output rows per tile
@@ -131,19 +132,35 @@ __device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or
   }
 }
 
-// Value at k-1 / k+1 (periodic in k: the warp holds the whole row).
-template <class T, int K>
-__device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, int lane) {
+// Value at k-1 / k+1 of a lane vector. The warp holds NS consecutive
+// segments of 32*K cells per row; inside a segment the neighbour is one
+// shuffle away, and with NS == 1 the shuffle also closes the periodic k wrap.
+// With NS > 1 the segment-edge lane reloads its single neighbour from the
+// vector's source row (global read-only path when G, shared memory else).
+template <int L, int NS, bool G, class T, int K>
+__device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, const T* row, int k0, int lane) {
   Vec<T, K> r;
   r.e[0] = __shfl_sync(kFull, a.e[K - 1], (lane + 31) & 31);
+  if constexpr (NS > 1) {
+    if (lane == 0) {
+      const T* p = row + (k0 == 0 ? L - 1 : k0 - 1);
+      r.e[0] = G ? __ldg(p) : *p;
+    }
+  }
 #pragma unroll
   for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
   return r;
 }
-template <class T, int K>
-__device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, int lane) {
+template <int L, int NS, bool G, class T, int K>
+__device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, const T* row, int k0, int lane) {
   Vec<T, K> r;
   r.e[K - 1] = __shfl_sync(kFull, a.e[0], (lane + 1) & 31);
+  if constexpr (NS > 1) {
+    if (lane == 31) {
+      const T* p = row + (k0 + K == L ? 0 : k0 + K);
+      r.e[K - 1] = G ? __ldg(p) : *p;
+    }
+  }
 #pragma unroll
   for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
   return r;
@@ -218,10 +235,10 @@ __device__ __forceinline__ T pseudo_face(T Un, T hL, T hR, T aR, T aL, T bp, T b
   }
 }
 
-template <class T, int L, int RW, int NW, bool NONOS>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RW, NW, NONOS>;
-  constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE;
+  using C = Cfg<T, L, RW, NW, NS, NONOS>;
+  constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS;
   using V = Vec<T, K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -240,24 +257,29 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   const int j0 = tile * C::TJ;
   const int m = a.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kl = lane * K;  // first k of this lane
 
-  // Rows of this warp: region row r = warp*RW + rr; global offsets of the
-  // row (j wraps periodically) and of its j-1 / j+1 neighbours.
+  // Rows of this warp: region row r = warp*RW + rr; global row offsets (j
+  // wraps periodically) of the row and its j-1 / j+1 neighbours.
   int gj[RW], gjm[RW], gjp[RW];
 #pragma unroll
   for (int rr = 0; rr < RW; ++rr) {
     int j = j0 - C::HALO + warp * RW + rr;
     j = ((j % m) + m) % m;
-    gj[rr] = j * L + kl;
-    gjm[rr] = (j == 0 ? m - 1 : j - 1) * L + kl;
-    gjp[rr] = (j == m - 1 ? 0 : j + 1) * L + kl;
+    gj[rr] = j * L;
+    gjm[rr] = (j == 0 ? m - 1 : j - 1) * L;
+    gjp[rr] = (j == m - 1 ? 0 : j + 1) * L;
   }
   auto slot3 = [](int p) { return (p + 6) % 3; };  // p >= -3
   auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
-  auto srow = [&](int r) { return r * L + kl; };  // smem offset of a row vector
+  // cell group c = (row rr, segment sg): first k of this lane in the segment
+  auto k0of = [&](int c) { return (c % NS) * 32 * K + lane * K; };
+  // neighbour helpers: G = global source row, S = shared source row
+#define KMG(vec, row, k0) kminus<L, NS, true>(vec, row, k0, lane)
+#define KPG(vec, row, k0) kplus<L, NS, true>(vec, row, k0, lane)
+#define KMS(vec, row, k0) kminus<L, NS, false>(vec, row, k0, lane)
+#define KPS(vec, row, k0) kplus<L, NS, false>(vec, row, k0, lane)
 
-  V nmx_new[RW], nmn_new[RW], nmx[RW], nmn[RW];  // psi^n star extrema (NONOS)
+  V nmx_new[NC], nmn_new[NC], nmx[NC], nmn[NC];  // psi^n star extrema (STARC)
 
   // P1: psi^(1) at plane p (donor cell) for all region rows.
   auto stage_donor = [&](int p) {
@@ -271,37 +293,39 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     const T* H = a.h + pl(p);
     T* dst = s_x1 + slot3(p) * PL;
 #pragma unroll
-    for (int rr = 0; rr < RW; ++rr) {
+    for (int c = 0; c < NC; ++c) {
+      const int rr = c / NS, k0 = k0of(c);
       const int r = warp * RW + rr;
-      const V xc = vload<T, K>(X + gj[rr]);
-      const V xm = vload<T, K>(Xm + gj[rr]), xp = vload<T, K>(Xp + gj[rr]);
-      const V ym = vload<T, K>(X + gjm[rr]), yp = vload<T, K>(X + gjp[rr]);
-      const V zm = kminus(xc, lane), zp = kplus(xc, lane);
-      const V uc = vload<T, K>(U + gj[rr]), up = vload<T, K>(Up + gj[rr]);
-      const V vc = vload<T, K>(Vv + gj[rr]), vp = vload<T, K>(Vv + gjp[rr]);
-      const V wc = vload<T, K>(W + gj[rr]);
-      const V wp = kplus(wc, lane);
-      const V hc = vload<T, K>(H + gj[rr]);
+      const int g = gj[rr] + k0;
+      const V xc = vload<T, K>(X + g);
+      const V xm = vload<T, K>(Xm + g), xp = vload<T, K>(Xp + g);
+      const V ym = vload<T, K>(X + gjm[rr] + k0), yp = vload<T, K>(X + gjp[rr] + k0);
+      const V zm = KMG(xc, X + gj[rr], k0), zp = KPG(xc, X + gj[rr], k0);
+      const V uc = vload<T, K>(U + g), up = vload<T, K>(Up + g);
+      const V vc = vload<T, K>(Vv + g), vp = vload<T, K>(Vv + gjp[rr] + k0);
+      const V wc = vload<T, K>(W + g);
+      const V wp = KPG(wc, W + gj[rr], k0);
+      const V hc = vload<T, K>(H + g);
       V res;
 #pragma unroll
       for (int e = 0; e < K; ++e) {
-        const T c = xc.e[e];
-        const T fxl = upflux(xm.e[e], c, uc.e[e]);
-        const T fxr = upflux(c, xp.e[e], up.e[e]);
-        const T fyl = upflux(ym.e[e], c, vc.e[e]);
-        const T fyr = upflux(c, yp.e[e], vp.e[e]);
-        const T fzl = upflux(zm.e[e], c, wc.e[e]);
-        const T fzr = upflux(c, zp.e[e], wp.e[e]);
+        const T x0 = xc.e[e];
+        const T fxl = upflux(xm.e[e], x0, uc.e[e]);
+        const T fxr = upflux(x0, xp.e[e], up.e[e]);
+        const T fyl = upflux(ym.e[e], x0, vc.e[e]);
+        const T fyr = upflux(x0, yp.e[e], vp.e[e]);
+        const T fzl = upflux(zm.e[e], x0, wc.e[e]);
+        const T fzr = upflux(x0, zp.e[e], wp.e[e]);
         const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-        res.e[e] = c - qdiv(div, hc.e[e]);
-        if constexpr (NONOS) {
-          nmx_new[rr].e[e] = tmax(tmax(tmax(c, xm.e[e]), tmax(xp.e[e], ym.e[e])),
-                                  tmax(tmax(yp.e[e], zm.e[e]), zp.e[e]));
-          nmn_new[rr].e[e] = tmin(tmin(tmin(c, xm.e[e]), tmin(xp.e[e], ym.e[e])),
-                                  tmin(tmin(yp.e[e], zm.e[e]), zp.e[e]));
+        res.e[e] = x0 - qdiv(div, hc.e[e]);
+        if constexpr (NONOS && STARC) {
+          nmx_new[c].e[e] = tmax(tmax(tmax(x0, xm.e[e]), tmax(xp.e[e], ym.e[e])),
+                                 tmax(tmax(yp.e[e], zm.e[e]), zp.e[e]));
+          nmn_new[c].e[e] = tmin(tmin(tmin(x0, xm.e[e]), tmin(xp.e[e], ym.e[e])),
+                                 tmin(tmin(yp.e[e], zm.e[e]), zp.e[e]));
         }
       }
-      vstore(dst + srow(r), res);
+      vstore(dst + r * L + k0, res);
     }
   };
 
@@ -320,90 +344,141 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     const T* H1 = a.h + pl(pb);
     const T* H2 = a.h + pl(pb + 1);
 #pragma unroll
-    for (int rr = 0; rr < RW; ++rr) {
+    for (int c = 0; c < NC; ++c) {
+      const int rr = c / NS, k0 = k0of(c);
       const int r = warp * RW + rr;
       if (r < 1) continue;  // warp-uniform
       const bool row_u = r < RR - 1;  // x/z faces (y faces: every r >= 1)
-      const V a1 = vabs(sload<T, K>(s1 + srow(r)));
-      const V a1m = vabs(sload<T, K>(s1 + srow(r - 1)));
-      const V u2c = vload<T, K>(U2 + gj[rr]);
-      const V h1c = vload<T, K>(H1 + gj[rr]);
-      const V a1km = kminus(a1, lane);
+      const int g = gj[rr] + k0;
+      const int so = r * L + k0;  // smem offset of this vector
+      const V x1 = sload<T, K>(s1 + so);
+      const V a1 = vabs(x1);
+      const V a1m = vabs(sload<T, K>(s1 + so - L));
+      const V u2c = vload<T, K>(U2 + g);
+      const V h1c = vload<T, K>(H1 + g);
+      const V a1km = vabs(KMS(x1, s1 + r * L, k0));
       if (row_u) {  // x-face between planes pb and pb+1 of this column
-        const V a2 = vabs(sload<T, K>(s2 + srow(r)));
-        const V a1p = vabs(sload<T, K>(s1 + srow(r + 1)));
-        const V a2p = vabs(sload<T, K>(s2 + srow(r + 1)));
-        const V a2m = vabs(sload<T, K>(s2 + srow(r - 1)));
-        const V a1kp = kplus(a1, lane), a2kp = kplus(a2, lane), a2km = kminus(a2, lane);
-        const V v1 = vload<T, K>(V1 + gj[rr]), v2 = vload<T, K>(V2 + gj[rr]);
-        const V v1p = vload<T, K>(V1 + gjp[rr]), v2p = vload<T, K>(V2 + gjp[rr]);
-        const V w1 = vload<T, K>(W1 + gj[rr]), w2 = vload<T, K>(W2 + gj[rr]);
-        const V w1p = kplus(w1, lane), w2p = kplus(w2, lane);
-        const V h2 = vload<T, K>(H2 + gj[rr]);
+        const V x2 = sload<T, K>(s2 + so);
+        const V a2 = vabs(x2);
+        const V a1kp = vabs(KPS(x1, s1 + r * L, k0));
+        const V a2kp = vabs(KPS(x2, s2 + r * L, k0)), a2km = vabs(KMS(x2, s2 + r * L, k0));
+        V bp, bm, cp, cm, Vs, Ws;
+        {
+          const V a1p = vabs(sload<T, K>(s1 + so + L)), a2p = vabs(sload<T, K>(s2 + so + L));
+          const V a2m = vabs(sload<T, K>(s2 + so - L));
 #pragma unroll
-        for (int e = 0; e < K; ++e) {
-          const T Vs = (v1.e[e] + v2.e[e]) + (v1p.e[e] + v2p.e[e]);
-          const T Ws = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
-          ut[rr].e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e],
-                                       a1p.e[e] + a2p.e[e], a1m.e[e] + a2m.e[e], Vs,
-                                       a1kp.e[e] + a2kp.e[e], a1km.e[e] + a2km.e[e], Ws);
+          for (int e = 0; e < K; ++e) {
+            bp.e[e] = a1p.e[e] + a2p.e[e];
+            bm.e[e] = a1m.e[e] + a2m.e[e];
+            cp.e[e] = a1kp.e[e] + a2kp.e[e];
+            cm.e[e] = a1km.e[e] + a2km.e[e];
+          }
         }
+        {
+          const V v1 = vload<T, K>(V1 + g), v2 = vload<T, K>(V2 + g);
+          const V v1p = vload<T, K>(V1 + gjp[rr] + k0), v2p = vload<T, K>(V2 + gjp[rr] + k0);
+#pragma unroll
+          for (int e = 0; e < K; ++e) Vs.e[e] = (v1.e[e] + v2.e[e]) + (v1p.e[e] + v2p.e[e]);
+        }
+        {
+          const V w1 = vload<T, K>(W1 + g), w2 = vload<T, K>(W2 + g);
+          const V w1p = KPG(w1, W1 + gj[rr], k0), w2p = KPG(w2, W2 + gj[rr], k0);
+#pragma unroll
+          for (int e = 0; e < K; ++e) Ws.e[e] = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
+        }
+        const V h2 = vload<T, K>(H2 + g);
+#pragma unroll
+        for (int e = 0; e < K; ++e)
+          ut[c].e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e], bp.e[e],
+                                      bm.e[e], Vs.e[e], cp.e[e], cm.e[e], Ws.e[e]);
       }
       if (only_u) continue;
-      const V a0 = vabs(sload<T, K>(s0 + srow(r)));
-      const V a2 = vabs(sload<T, K>(s2 + srow(r)));
-      const V u1c = vload<T, K>(U1 + gj[rr]);
-      const V w1 = vload<T, K>(W1 + gj[rr]);
+      const V x0 = sload<T, K>(s0 + so);
+      const V x2 = sload<T, K>(s2 + so);
+      const V u1c = vload<T, K>(U1 + g);
+      const V w1 = vload<T, K>(W1 + g);
       {  // y-face between rows r-1 and r of plane pb
-        const V a0m = vabs(sload<T, K>(s0 + srow(r - 1)));
-        const V a2m = vabs(sload<T, K>(s2 + srow(r - 1)));
-        const V a1mkp = kplus(a1m, lane), a1mkm = kminus(a1m, lane), a1kp = kplus(a1, lane);
-        const V u1m = vload<T, K>(U1 + gjm[rr]), u2m = vload<T, K>(U2 + gjm[rr]);
-        const V w1m = vload<T, K>(W1 + gjm[rr]);
-        const V w1mkp = kplus(w1m, lane), w1kp = kplus(w1, lane);
-        const V v1 = vload<T, K>(V1 + gj[rr]);
-        const V h1m = vload<T, K>(H1 + gjm[rr]);
+        const V x1m = sload<T, K>(s1 + so - L);
+        V bp, bm, cp, cm, Us, Ws;
+        {
+          const V a0m = vabs(sload<T, K>(s0 + so - L)), a2m = vabs(sload<T, K>(s2 + so - L));
+          const V a1mkp = vabs(KPS(x1m, s1 + (r - 1) * L, k0));
+          const V a1mkm = vabs(KMS(x1m, s1 + (r - 1) * L, k0));
+          const V a1kp = vabs(KPS(x1, s1 + r * L, k0));
+#pragma unroll
+          for (int e = 0; e < K; ++e) {
+            bp.e[e] = a2m.e[e] + fabs(x2.e[e]);
+            bm.e[e] = a0m.e[e] + fabs(x0.e[e]);
+            cp.e[e] = a1mkp.e[e] + a1kp.e[e];
+            cm.e[e] = a1mkm.e[e] + a1km.e[e];
+          }
+        }
+        {
+          const V u1m = vload<T, K>(U1 + gjm[rr] + k0), u2m = vload<T, K>(U2 + gjm[rr] + k0);
+#pragma unroll
+          for (int e = 0; e < K; ++e) Us.e[e] = (u1m.e[e] + u1c.e[e]) + (u2m.e[e] + u2c.e[e]);
+        }
+        {
+          const V w1m = vload<T, K>(W1 + gjm[rr] + k0);
+          const V w1mkp = KPG(w1m, W1 + gjm[rr], k0), w1kp = KPG(w1, W1 + gj[rr], k0);
+#pragma unroll
+          for (int e = 0; e < K; ++e) Ws.e[e] = (w1m.e[e] + w1.e[e]) + (w1mkp.e[e] + w1kp.e[e]);
+        }
+        const V v1 = vload<T, K>(V1 + g);
+        const V h1m = vload<T, K>(H1 + gjm[rr] + k0);
         V res;
 #pragma unroll
-        for (int e = 0; e < K; ++e) {
-          const T Us = (u1m.e[e] + u1c.e[e]) + (u2m.e[e] + u2c.e[e]);
-          const T Ws = (w1m.e[e] + w1.e[e]) + (w1mkp.e[e] + w1kp.e[e]);
-          res.e[e] = pseudo_face<T>(v1.e[e], h1m.e[e], h1c.e[e], a1.e[e], a1m.e[e],
-                                    a2m.e[e] + a2.e[e], a0m.e[e] + a0.e[e], Us,
-                                    a1mkp.e[e] + a1kp.e[e], a1mkm.e[e] + a1km.e[e], Ws);
-        }
-        vstore(vdst + srow(r), res);
+        for (int e = 0; e < K; ++e)
+          res.e[e] = pseudo_face<T>(v1.e[e], h1m.e[e], h1c.e[e], a1.e[e], a1m.e[e], bp.e[e],
+                                    bm.e[e], Us.e[e], cp.e[e], cm.e[e], Ws.e[e]);
+        vstore(vdst + so, res);
       }
       if (row_u) {  // z-face between k-1 and k
-        const V a1p = vabs(sload<T, K>(s1 + srow(r + 1)));
-        const V a1pkm = kminus(a1p, lane), a1mkm = kminus(a1m, lane);
-        const V a2km = kminus(a2, lane), a0km = kminus(a0, lane);
-        const V u2km = kminus(u2c, lane), u1km = kminus(u1c, lane);
-        const V v1 = vload<T, K>(V1 + gj[rr]), v1p = vload<T, K>(V1 + gjp[rr]);
-        const V v1km = kminus(v1, lane), v1pkm = kminus(v1p, lane);
-        const V h1km = kminus(h1c, lane);
+        V bp, bm, cp, cm, Us, Vs;
+        {
+          const V x1p = sload<T, K>(s1 + so + L);
+          const V x1m = sload<T, K>(s1 + so - L);
+          const V a1pkm = vabs(KMS(x1p, s1 + (r + 1) * L, k0));
+          const V a1mkm = vabs(KMS(x1m, s1 + (r - 1) * L, k0));
+          const V a2km = vabs(KMS(x2, s2 + r * L, k0)), a0km = vabs(KMS(x0, s0 + r * L, k0));
+#pragma unroll
+          for (int e = 0; e < K; ++e) {
+            bp.e[e] = a2km.e[e] + fabs(x2.e[e]);
+            bm.e[e] = a0km.e[e] + fabs(x0.e[e]);
+            cp.e[e] = a1pkm.e[e] + fabs(x1p.e[e]);
+            cm.e[e] = a1mkm.e[e] + a1m.e[e];
+          }
+        }
+        {
+          const V u2km = KMG(u2c, U2 + gj[rr], k0), u1km = KMG(u1c, U1 + gj[rr], k0);
+#pragma unroll
+          for (int e = 0; e < K; ++e) Us.e[e] = (u1km.e[e] + u1c.e[e]) + (u2km.e[e] + u2c.e[e]);
+        }
+        {
+          const V v1 = vload<T, K>(V1 + g), v1p = vload<T, K>(V1 + gjp[rr] + k0);
+          const V v1km = KMG(v1, V1 + gj[rr], k0), v1pkm = KMG(v1p, V1 + gjp[rr], k0);
+#pragma unroll
+          for (int e = 0; e < K; ++e) Vs.e[e] = (v1km.e[e] + v1.e[e]) + (v1pkm.e[e] + v1p.e[e]);
+        }
+        const V h1km = KMG(h1c, H1 + gj[rr], k0);
         V res;
 #pragma unroll
-        for (int e = 0; e < K; ++e) {
-          const T Us = (u1km.e[e] + u1c.e[e]) + (u2km.e[e] + u2c.e[e]);
-          const T Vs = (v1km.e[e] + v1.e[e]) + (v1pkm.e[e] + v1p.e[e]);
-          res.e[e] = pseudo_face<T>(w1.e[e], h1km.e[e], h1c.e[e], a1.e[e], a1km.e[e],
-                                    a2km.e[e] + a2.e[e], a0km.e[e] + a0.e[e], Us,
-                                    a1pkm.e[e] + a1p.e[e], a1mkm.e[e] + a1m.e[e], Vs);
-        }
-        vstore(wdst + srow(r), res);
+        for (int e = 0; e < K; ++e)
+          res.e[e] = pseudo_face<T>(w1.e[e], h1km.e[e], h1c.e[e], a1.e[e], a1km.e[e], bp.e[e],
+                                    bm.e[e], Us.e[e], cp.e[e], cm.e[e], Vs.e[e]);
+        vstore(wdst + so, res);
       }
     }
   };
 
   // ---- register carries along i (same (j,k) column) -------------------------
-  V ucar[RW], ufresh[RW], fxc[RW];
+  V ucar[NC], ufresh[NC], fxc[NC];
 #pragma unroll
-  for (int rr = 0; rr < RW; ++rr)
+  for (int c = 0; c < NC; ++c)
 #pragma unroll
     for (int e = 0; e < K; ++e) {
-      ucar[rr].e[e] = ufresh[rr].e[e] = fxc[rr].e[e] = T(0);
-      nmx[rr].e[e] = nmn[rr].e[e] = nmx_new[rr].e[e] = nmn_new[rr].e[e] = T(0);
+      ucar[c].e[e] = ufresh[c].e[e] = fxc[c].e[e] = T(0);
+      nmx[c].e[e] = nmn[c].e[e] = nmx_new[c].e[e] = nmn_new[c].e[e] = T(0);
     }
 
   const int lag = NONOS ? 2 : 1;  // psi^(1) planes ahead of the output plane
@@ -411,11 +486,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // pseudo-velocity between them.
   stage_donor(ib - lag);
   stage_donor(ib - lag + 1);
-  if constexpr (NONOS) {
+  if constexpr (NONOS && STARC) {
 #pragma unroll
-    for (int rr = 0; rr < RW; ++rr) {
-      nmx[rr] = nmx_new[rr];
-      nmn[rr] = nmn_new[rr];
+    for (int c = 0; c < NC; ++c) {
+      nmx[c] = nmx_new[c];
+      nmn[c] = nmn_new[c];
     }
   }
   __syncthreads();
@@ -444,32 +519,55 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const T* s1 = s_x1 + slot3(t + 1) * PL;
         const T* s2 = s_x1 + slot3(t + 2) * PL;
         const T* H1 = a.h + pl(p1);
+        const T* Xn0 = a.x + pl(t);
+        const T* Xn1 = a.x + pl(p1);
+        const T* Xn2 = a.x + pl(t + 2);
 #pragma unroll
-        for (int rr = 0; rr < RW; ++rr) {
+        for (int c = 0; c < NC; ++c) {
+          const int rr = c / NS, k0 = k0of(c);
           const int r = warp * RW + rr;
           if (r < 1 || r >= RR - 1) continue;
-          const V xc = sload<T, K>(s1 + srow(r));
-          const V xm = sload<T, K>(s0 + srow(r)), xp = sload<T, K>(s2 + srow(r));
-          const V ym = sload<T, K>(s1 + srow(r - 1)), yp = sload<T, K>(s1 + srow(r + 1));
-          const V zm = kminus(xc, lane), zp = kplus(xc, lane);
-          const V va = sload<T, K>(vA + srow(r)), vap = sload<T, K>(vA + srow(r + 1));
-          const V wa = sload<T, K>(wA + srow(r));
-          const V wap = kplus(wa, lane);
-          const V hc = vload<T, K>(H1 + gj[rr]);
+          const int so = r * L + k0;
+          const V xc = sload<T, K>(s1 + so);
+          const V xm = sload<T, K>(s0 + so), xp = sload<T, K>(s2 + so);
+          const V ym = sload<T, K>(s1 + so - L), yp = sload<T, K>(s1 + so + L);
+          const V zm = KMS(xc, s1 + r * L, k0), zp = KPS(xc, s1 + r * L, k0);
+          V mx, mn;
+          if constexpr (STARC) {
+            mx = nmx[c];
+            mn = nmn[c];
+          } else {  // psi^n star of plane t+1, reloaded
+            const int g = gj[rr] + k0;
+            const V nc = vload<T, K>(Xn1 + g);
+            const V n0 = vload<T, K>(Xn0 + g), n2 = vload<T, K>(Xn2 + g);
+            const V nym = vload<T, K>(Xn1 + gjm[rr] + k0), nyp = vload<T, K>(Xn1 + gjp[rr] + k0);
+            const V nzm = KMG(nc, Xn1 + gj[rr], k0), nzp = KPG(nc, Xn1 + gj[rr], k0);
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+              mx.e[e] = tmax(tmax(tmax(nc.e[e], n0.e[e]), tmax(n2.e[e], nym.e[e])),
+                             tmax(tmax(nyp.e[e], nzm.e[e]), nzp.e[e]));
+              mn.e[e] = tmin(tmin(tmin(nc.e[e], n0.e[e]), tmin(n2.e[e], nym.e[e])),
+                             tmin(tmin(nyp.e[e], nzm.e[e]), nzp.e[e]));
+            }
+          }
+          const V va = sload<T, K>(vA + so), vap = sload<T, K>(vA + so + L);
+          const V wa = sload<T, K>(wA + so);
+          const V wap = KPS(wa, wA + r * L, k0);
+          const V hc = vload<T, K>(H1 + gj[rr] + k0);
           V bu, bd;
 #pragma unroll
           for (int e = 0; e < K; ++e) {
-            const T c = xc.e[e];
-            const T mx = tmax(tmax(tmax(nmx[rr].e[e], c), tmax(xm.e[e], xp.e[e])),
+            const T x0 = xc.e[e];
+            const T hi = tmax(tmax(tmax(mx.e[e], x0), tmax(xm.e[e], xp.e[e])),
                               tmax(tmax(ym.e[e], yp.e[e]), tmax(zm.e[e], zp.e[e])));
-            const T mn = tmin(tmin(tmin(nmn[rr].e[e], c), tmin(xm.e[e], xp.e[e])),
+            const T lo = tmin(tmin(tmin(mn.e[e], x0), tmin(xm.e[e], xp.e[e])),
                               tmin(tmin(ym.e[e], yp.e[e]), tmin(zm.e[e], zp.e[e])));
-            const T axl = upflux(xm.e[e], c, ucar[rr].e[e]);
-            const T axr = upflux(c, xp.e[e], ufresh[rr].e[e]);
-            const T ayl = upflux(ym.e[e], c, va.e[e]);
-            const T ayr = upflux(c, yp.e[e], vap.e[e]);
-            const T azl = upflux(zm.e[e], c, wa.e[e]);
-            const T azr = upflux(c, zp.e[e], wap.e[e]);
+            const T axl = upflux(xm.e[e], x0, ucar[c].e[e]);
+            const T axr = upflux(x0, xp.e[e], ufresh[c].e[e]);
+            const T ayl = upflux(ym.e[e], x0, va.e[e]);
+            const T ayr = upflux(x0, yp.e[e], vap.e[e]);
+            const T azl = upflux(zm.e[e], x0, wa.e[e]);
+            const T azr = upflux(x0, zp.e[e], wap.e[e]);
             // 2*pos(f) = f + |f| and -2*neg(f) = |f| - f are exact, so these
             // are the oracle's inflow/outflow sums scaled by exactly 2.
             const T fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) +
@@ -481,15 +579,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const T di = T(0.5) * fin2 + Eps<T>::value, dou = T(0.5) * fout2 + Eps<T>::value;
             if constexpr (sizeof(T) == 8) {
               const T rr2 = rcp(di * dou);
-              bu.e[e] = ((mx - c) * hc.e[e]) * dou * rr2;
-              bd.e[e] = ((c - mn) * hc.e[e]) * di * rr2;
+              bu.e[e] = ((hi - x0) * hc.e[e]) * dou * rr2;
+              bd.e[e] = ((x0 - lo) * hc.e[e]) * di * rr2;
             } else {
-              bu.e[e] = qdiv((mx - c) * hc.e[e], di);
-              bd.e[e] = qdiv((c - mn) * hc.e[e], dou);
+              bu.e[e] = qdiv((hi - x0) * hc.e[e], di);
+              bd.e[e] = qdiv((x0 - lo) * hc.e[e], dou);
             }
           }
-          vstore(buA + srow(r), bu);
-          vstore(bdA + srow(r), bd);
+          vstore(buA + so, bu);
+          vstore(bdA + so, bd);
         }
       }
       __syncthreads();
@@ -500,62 +598,70 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const T* H0 = a.h + pl(t);
         T* O = a.out + pl(t);
 #pragma unroll
-        for (int rr = 0; rr < RW; ++rr) {
+        for (int c = 0; c < NC; ++c) {
+          const int rr = c / NS, k0 = k0of(c);
           const int r = warp * RW + rr;
           if (r < 2 || r >= RR - 1) continue;
-          const V bu = sload<T, K>(buA + srow(r)), bd = sload<T, K>(bdA + srow(r));
+          const int so = r * L + k0;
+          const V bu = sload<T, K>(buA + so), bd = sload<T, K>(bdA + so);
           {
-            const V va = sload<T, K>(vA + srow(r));
-            const V bum = sload<T, K>(buA + srow(r - 1)), bdm = sload<T, K>(bdA + srow(r - 1));
+            const V va = sload<T, K>(vA + so);
+            const V bum = sload<T, K>(buA + so - L), bdm = sload<T, K>(bdA + so - L);
             V res;
 #pragma unroll
             for (int e = 0; e < K; ++e)
               res.e[e] = limit_sel(va.e[e], bdm.e[e], bu.e[e], bum.e[e], bd.e[e]);
-            vstore(vA + srow(r), res);
+            vstore(vA + so, res);
           }
           if (r >= RR - 2) continue;
-          const V wa = sload<T, K>(wA + srow(r));
-          const V bukm = kminus(bu, lane), bdkm = kminus(bd, lane);
-          const V buo = sload<T, K>(buB + srow(r)), bdo = sload<T, K>(bdB + srow(r));
-          const V xc = sload<T, K>(s0 + srow(r));
-          const V x1 = sload<T, K>(s1 + srow(r));
-          V wres, fxr;
+          V fxr;
+          {
+            const V wa = sload<T, K>(wA + so);
+            const V bukm = KMS(bu, buA + r * L, k0), bdkm = KMS(bd, bdA + r * L, k0);
+            const V buo = sload<T, K>(buB + so), bdo = sload<T, K>(bdB + so);
+            const V xc = sload<T, K>(s0 + so);
+            const V x1 = sload<T, K>(s1 + so);
+            V wres;
 #pragma unroll
-          for (int e = 0; e < K; ++e) {
-            wres.e[e] = limit_sel(wa.e[e], bdkm.e[e], bu.e[e], bukm.e[e], bd.e[e]);
-            const T ul = limit_sel(ucar[rr].e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
-            fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
+            for (int e = 0; e < K; ++e) {
+              wres.e[e] = limit_sel(wa.e[e], bdkm.e[e], bu.e[e], bukm.e[e], bd.e[e]);
+              const T ul = limit_sel(ucar[c].e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
+              fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
+            }
+            vstore(wA + so, wres);
           }
-          vstore(wA + srow(r), wres);
           if (emit) {
-            const V ym = sload<T, K>(s0 + srow(r - 1)), yp = sload<T, K>(s0 + srow(r + 1));
-            const V zm = kminus(xc, lane), zp = kplus(xc, lane);
-            const V vb = sload<T, K>(vB + srow(r)), vbp = sload<T, K>(vB + srow(r + 1));
-            const V wb = sload<T, K>(wB + srow(r));
-            const V wbp = kplus(wb, lane);
-            const V hc = vload<T, K>(H0 + gj[rr]);
+            const V xc = sload<T, K>(s0 + so);
+            const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
+            const V zm = KMS(xc, s0 + r * L, k0), zp = KPS(xc, s0 + r * L, k0);
+            const V vb = sload<T, K>(vB + so), vbp = sload<T, K>(vB + so + L);
+            const V wb = sload<T, K>(wB + so);
+            const V wbp = KPS(wb, wB + r * L, k0);
+            const V hc = vload<T, K>(H0 + gj[rr] + k0);
             V res;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
-              const T c = xc.e[e];
-              const T fyl = upflux(ym.e[e], c, vb.e[e]);
-              const T fyr = upflux(c, yp.e[e], vbp.e[e]);
-              const T fzl = upflux(zm.e[e], c, wb.e[e]);
-              const T fzr = upflux(c, zp.e[e], wbp.e[e]);
-              const T div = ((fxr.e[e] - fxc[rr].e[e]) + (fyr - fyl)) + (fzr - fzl);
-              res.e[e] = c - qdiv(div, hc.e[e]);
+              const T x0 = xc.e[e];
+              const T fyl = upflux(ym.e[e], x0, vb.e[e]);
+              const T fyr = upflux(x0, yp.e[e], vbp.e[e]);
+              const T fzl = upflux(zm.e[e], x0, wb.e[e]);
+              const T fzr = upflux(x0, zp.e[e], wbp.e[e]);
+              const T div = ((fxr.e[e] - fxc[c].e[e]) + (fyr - fyl)) + (fzr - fzl);
+              res.e[e] = x0 - qdiv(div, hc.e[e]);
             }
             const int j = j0 + r - 2;
-            if (j < m) vstore(O + gj[rr], res);
+            if (j < m) vstore(O + gj[rr] + k0, res);
           }
-          fxc[rr] = fxr;
+          fxc[c] = fxr;
         }
       }
 #pragma unroll
-      for (int rr = 0; rr < RW; ++rr) {
-        ucar[rr] = ufresh[rr];
-        nmx[rr] = nmx_new[rr];
-        nmn[rr] = nmn_new[rr];
+      for (int c = 0; c < NC; ++c) {
+        ucar[c] = ufresh[c];
+        if constexpr (STARC) {
+          nmx[c] = nmx_new[c];
+          nmn[c] = nmn_new[c];
+        }
       }
       __syncthreads();
     } else {
@@ -568,37 +674,43 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const T* H0 = a.h + pl(t);
       T* O = a.out + pl(t);
 #pragma unroll
-      for (int rr = 0; rr < RW; ++rr) {
+      for (int c = 0; c < NC; ++c) {
+        const int rr = c / NS, k0 = k0of(c);
         const int r = warp * RW + rr;
         if (r < 1 || r >= RR - 1) continue;
-        const V xc = sload<T, K>(s0 + srow(r));
-        const V xm = sload<T, K>(sm1 + srow(r)), xp = sload<T, K>(s1 + srow(r));
-        const V ym = sload<T, K>(s0 + srow(r - 1)), yp = sload<T, K>(s0 + srow(r + 1));
-        const V zm = kminus(xc, lane), zp = kplus(xc, lane);
-        const V vv = sload<T, K>(s_v + srow(r)), vvp = sload<T, K>(s_v + srow(r + 1));
-        const V ww = sload<T, K>(s_w + srow(r));
-        const V wwp = kplus(ww, lane);
-        const V hc = vload<T, K>(H0 + gj[rr]);
+        const int so = r * L + k0;
+        const V xc = sload<T, K>(s0 + so);
+        const V xm = sload<T, K>(sm1 + so), xp = sload<T, K>(s1 + so);
+        const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
+        const V zm = KMS(xc, s0 + r * L, k0), zp = KPS(xc, s0 + r * L, k0);
+        const V vv = sload<T, K>(s_v + so), vvp = sload<T, K>(s_v + so + L);
+        const V ww = sload<T, K>(s_w + so);
+        const V wwp = KPS(ww, s_w + r * L, k0);
+        const V hc = vload<T, K>(H0 + gj[rr] + k0);
         V res;
 #pragma unroll
         for (int e = 0; e < K; ++e) {
-          const T c = xc.e[e];
-          const T fxl = upflux(xm.e[e], c, ucar[rr].e[e]);
-          const T fxr = upflux(c, xp.e[e], ufresh[rr].e[e]);
-          const T fyl = upflux(ym.e[e], c, vv.e[e]);
-          const T fyr = upflux(c, yp.e[e], vvp.e[e]);
-          const T fzl = upflux(zm.e[e], c, ww.e[e]);
-          const T fzr = upflux(c, zp.e[e], wwp.e[e]);
+          const T x0 = xc.e[e];
+          const T fxl = upflux(xm.e[e], x0, ucar[c].e[e]);
+          const T fxr = upflux(x0, xp.e[e], ufresh[c].e[e]);
+          const T fyl = upflux(ym.e[e], x0, vv.e[e]);
+          const T fyr = upflux(x0, yp.e[e], vvp.e[e]);
+          const T fzl = upflux(zm.e[e], x0, ww.e[e]);
+          const T fzr = upflux(x0, zp.e[e], wwp.e[e]);
           const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-          res.e[e] = c - qdiv(div, hc.e[e]);
+          res.e[e] = x0 - qdiv(div, hc.e[e]);
         }
         const int j = j0 + r - 1;
-        if (j < m) vstore(O + gj[rr], res);
-        ucar[rr] = ufresh[rr];
+        if (j < m) vstore(O + gj[rr] + k0, res);
+        ucar[c] = ufresh[c];
       }
       __syncthreads();
     }
   }
+#undef KMG
+#undef KPG
+#undef KMS
+#undef KPS
 }
 
 struct Plan {
@@ -623,16 +735,16 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   return best;
 }
 
-template <class T, int L, int RW, int NW, bool NONOS>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC>
 int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
                T* out, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RW, NW, NONOS>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
-    cudaFuncSetAttribute(k_fused<T, L, RW, NW, NONOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_fused<T, L, RW, NW, NS, NONOS, STARC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RW, NW, NONOS>, C::NT,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RW, NW, NS, NONOS, STARC>, C::NT,
                                                   C::SMEM);
     if (per_sm < 1) per_sm = 1;
     configured = true;
@@ -640,17 +752,21 @@ int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T
   const Plan p = plan_grid(fs.m, C::TJ, fs.o1 - fs.o0, per_sm * num_sms, NONOS ? 4 : 2);
   Args<T> a{x, u, v, w, h, out, static_cast<int>(fs.m), static_cast<int>(fs.R), p.ntj, p.nseg,
             static_cast<int>(fs.o0), static_cast<int>(fs.o1), fs.m * fs.l};
-  k_fused<T, L, RW, NW, NONOS><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
+  k_fused<T, L, RW, NW, NS, NONOS, STARC><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
   return 1;
 }
 
 template <class T, bool NONOS>
 int dispatch_l(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
                T* out, int num_sms, cudaStream_t st) {
+  // fp64 keeps lane vectors at 2 doubles (register budget) and reloads the
+  // psi^n star; fp32 holds 4 floats per lane and carries the star.
+  constexpr bool D = sizeof(T) == 8;
   switch (fs.l) {
-    case 128: return launch_cfg<T, 128, 1, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-    case 64: return launch_cfg<T, 64, 2, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
-    case 32: return launch_cfg<T, 32, 4, 16, NONOS>(fs, x, u, v, w, h, out, num_sms, st);
+    case 128:
+      return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
+    case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
+    case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
     default: return 0;
   }
 }
