@@ -149,6 +149,7 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
   IMB_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
   IMB_CUDA(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming));
   IMB_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
+  IMB_CUDA(cudaEventCreateWithFlags(&ev_static_, cudaEventDisableTiming));
   const std::size_t fbytes = static_cast<std::size_t>(P_) * plane_bytes();
   const bool fused = dev::fused_supported(opt_.iord, opt_.nonos, m_, l_, opt_.fp64) &&
                      ni_ >= 2 * R_;
@@ -177,6 +178,7 @@ Team::~Team() {
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   if (ev_ready_) cudaEventDestroy(ev_ready_);
   if (ev_halo_) cudaEventDestroy(ev_halo_);
+  if (ev_static_) cudaEventDestroy(ev_static_);
   if (cs_) cudaStreamDestroy(cs_);
   if (xs_) cudaStreamDestroy(xs_);
   if (pool_) cudaFree(pool_);
@@ -275,14 +277,14 @@ void Team::exchange_static() {
   static_halo_ok_ = true;
 }
 
-void Team::pull_from_ring(int field) {
+void Team::pull_from_ring(int field, cudaStream_t st) {
   const std::size_t pb = plane_bytes(), bytes = pb * static_cast<std::size_t>(R_);
   char* mine = static_cast<char*>(fbuf(field));
   const char* lsrc = static_cast<const char*>(left_->fbuf(field)) + pb * static_cast<std::size_t>(left_->ni_);
   const char* rsrc = static_cast<const char*>(right_->fbuf(field)) + pb * static_cast<std::size_t>(right_->R_);
-  IMB_CUDA(cudaMemcpyPeerAsync(mine, device_, lsrc, left_->device_, bytes, cs_));
+  IMB_CUDA(cudaMemcpyPeerAsync(mine, device_, lsrc, left_->device_, bytes, st));
   IMB_CUDA(cudaMemcpyPeerAsync(mine + pb * static_cast<std::size_t>(R_ + ni_), device_, rsrc,
-                               right_->device_, bytes, cs_));
+                               right_->device_, bytes, st));
 }
 
 void Team::begin_compute_window() {
@@ -410,6 +412,42 @@ void Team::compute_step() {
     compute_step_t<float>();
 }
 
+// Fused step kernel over output planes [o0, o1) (interior coordinates), no swap.
+void Team::fused_range(std::int64_t o0, std::int64_t o1) {
+  if (o1 <= o0) return;
+  dev::FusedShape fs{m_, l_, ni_, R_, o0, o1};
+  if (opt_.fp64)
+    launches_ += dev::launch_fused<double>(
+        fs, opt_.iord, opt_.nonos, static_cast<const double*>(x_), static_cast<const double*>(st_[0]),
+        static_cast<const double*>(st_[1]), static_cast<const double*>(st_[2]),
+        static_cast<const double*>(st_[3]), static_cast<double*>(xn_), num_sms_, cs_);
+  else
+    launches_ += dev::launch_fused<float>(
+        fs, opt_.iord, opt_.nonos, static_cast<const float*>(x_), static_cast<const float*>(st_[0]),
+        static_cast<const float*>(st_[1]), static_cast<const float*>(st_[2]),
+        static_cast<const float*>(st_[3]), static_cast<float*>(xn_), num_sms_, cs_);
+  IMB_CUDA(cudaGetLastError());
+}
+
+// Multi-rank step with the halo exchange hidden behind the interior: the
+// interior output planes [R, ni-R) read no halo plane, so they run while NCCL
+// moves the halos on the exchange stream; the 2R boundary planes follow the
+// exchange event. The next step's sends read planes written by the boundary
+// launches, which the ev_ready record at the top of that step orders.
+void Team::step_overlapped() {
+  IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
+  IMB_CUDA(cudaStreamWaitEvent(xs_, ev_ready_, 0));
+  nccl_->swap_halos(static_cast<char*>(x_), plane_bytes(), R_, ni_, xs_);
+  IMB_CUDA(cudaEventRecord(ev_halo_, xs_));
+  begin_compute_window();
+  fused_range(R_, ni_ - R_);
+  IMB_CUDA(cudaStreamWaitEvent(cs_, ev_halo_, 0));
+  fused_range(0, R_);
+  fused_range(ni_ - R_, ni_);
+  end_compute_window();
+  std::swap(x_, xn_);
+}
+
 void Team::run(int steps, double* compute_s, double* wall_s) {
   if (steps < 0) throw ContractError("steps must be >= 0");
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
@@ -421,7 +459,12 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   IMB_CUDA(cudaEventRecord(t0, cs_));
   if (!static_halo_ok_) exchange_static();
   ev_used_ = 0;
+  const bool overlap = multi && tmp_[0] == nullptr && ni_ > 2 * R_;
   for (int s = 0; s < steps; ++s) {
+    if (overlap) {
+      step_overlapped();
+      continue;
+    }
     if (multi)
       exchange_x_nccl(x_);
     else
@@ -479,6 +522,7 @@ void Team::connect_nccl(const unsigned char* id, int nranks, int rank) {
 void Team::group_mark_ready() {
   IMB_CUDA(cudaSetDevice(device_));
   IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
+  IMB_CUDA(cudaEventRecord(ev_static_, cs_));
 }
 
 void Team::group_pull() {
@@ -486,16 +530,36 @@ void Team::group_pull() {
   IMB_CUDA(cudaStreamWaitEvent(cs_, left_->ev_ready_, 0));
   IMB_CUDA(cudaStreamWaitEvent(cs_, right_->ev_ready_, 0));
   if (!static_halo_ok_) {
-    for (int f = 1; f <= 4; ++f) pull_from_ring(f);
+    for (int f = 1; f <= 4; ++f) pull_from_ring(f, cs_);
     static_halo_ok_ = true;
   }
-  pull_from_ring(0);
+  group_overlap_ = tmp_[0] == nullptr && ni_ > 2 * R_;
+  if (!group_overlap_) {
+    pull_from_ring(0, cs_);
+    return;
+  }
+  // Same split as the NCCL path: the pull runs on the exchange stream after
+  // both neighbours and this team finished the previous step.
+  IMB_CUDA(cudaStreamWaitEvent(xs_, left_->ev_ready_, 0));
+  IMB_CUDA(cudaStreamWaitEvent(xs_, right_->ev_ready_, 0));
+  IMB_CUDA(cudaStreamWaitEvent(xs_, ev_ready_, 0));
+  IMB_CUDA(cudaStreamWaitEvent(xs_, ev_static_, 0));
+  pull_from_ring(0, xs_);
+  IMB_CUDA(cudaEventRecord(ev_halo_, xs_));
 }
 
 void Team::group_compute() {
   IMB_CUDA(cudaSetDevice(device_));
   begin_compute_window();
-  compute_step();
+  if (group_overlap_) {
+    fused_range(R_, ni_ - R_);
+    IMB_CUDA(cudaStreamWaitEvent(cs_, ev_halo_, 0));
+    fused_range(0, R_);
+    fused_range(ni_ - R_, ni_);
+    std::swap(x_, xn_);
+  } else {
+    compute_step();
+  }
   end_compute_window();
 }
 

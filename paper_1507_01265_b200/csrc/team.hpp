@@ -88,8 +88,10 @@ class Team {
   void exchange_static();
   void exchange_x_self(void* x);
   void exchange_x_nccl(void* x);
-  void pull_from_ring(int field_buf);
+  void pull_from_ring(int field, cudaStream_t st);
   void compute_step();  // x (halo-complete) -> xn, then swap
+  void fused_range(std::int64_t o0, std::int64_t o1);
+  void step_overlapped();  // NCCL exchange hidden behind the interior planes
   template <class T>
   void compute_step_t();
   void* fbuf(int field) const;
@@ -103,7 +105,8 @@ class Team {
   std::int64_t i0_, ni_, R_, P_;
   int num_sms_ = 148;
   cudaStream_t cs_ = nullptr, xs_ = nullptr;  // compute, exchange
-  cudaEvent_t ev_ready_ = nullptr, ev_halo_ = nullptr;
+  cudaEvent_t ev_ready_ = nullptr, ev_halo_ = nullptr, ev_static_ = nullptr;
+  bool group_overlap_ = false;
   std::vector<cudaEvent_t> ev_pool_;  // begin/end pairs of compute windows
   std::size_t ev_used_ = 0;
   // device buffers (padded slabs of P_ planes)
