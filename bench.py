@@ -244,15 +244,15 @@ def main():
     e2e_value = cells * args.e2e_steps / e2e_s / 1e9
 
     peak, peak_src = peaks()
-    traffic = None
+    bytes_per_cell = 6 * elem  # psi,u,v,w,h read + psi write (SURVEY.md §8d)
+    local_cells = shares[rank] * m * l
+    per_step = comp_max / args.steps
+    traffic = None  # DRAM bytes per launch from the committed ncu capture
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         rec = json.loads(tfile.read_text()).get(f"{args.config}/{'f64' if fp64 else 'f32'}")
         if rec and world == 1:
-            traffic = rec["dram_bytes_per_launch"] / 1e9 / per_step
-    bytes_per_cell = 6 * elem  # psi,u,v,w,h read + psi write (SURVEY.md §8d)
-    local_cells = shares[rank] * m * l
-    per_step = comp_max / args.steps
+            traffic = rec["dram_bytes_per_launch"]
     achieved = local_cells * bytes_per_cell / per_step / 1e9 if world == 1 else \
         max(shares) * m * l * bytes_per_cell / per_step / 1e9
 
@@ -270,8 +270,10 @@ def main():
                 "path": "imb_team_step_host (pinned host x in, step incl. halo exchange, x out)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_note": "ncu DRAM bytes per launch (profiles/traffic.json) / live "
-                                     "launch time, GB/s; null when not captured for this config",
+                     "traffic_note": "bytes per launch: ncu dram__bytes_read+write of the step "
+                                     "kernel (profiles/traffic.json); compare with "
+                                     "algorithmic_bytes_per_launch; null if not captured",
+                     "algorithmic_bytes_per_launch": local_cells * bytes_per_cell,
                      "kernel": ("k_fused (one launch per step; CUDA events on the team compute "
                                 "stream)" if iord == 2 and l in (32, 64, 128) else
                                 "staged step kernels (per-step compute window)"),

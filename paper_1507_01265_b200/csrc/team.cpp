@@ -181,6 +181,9 @@ Team::~Team() {
   if (ev_static_) cudaEventDestroy(ev_static_);
   if (cs_) cudaStreamDestroy(cs_);
   if (xs_) cudaStreamDestroy(xs_);
+  if (ups_) cudaStreamDestroy(ups_);
+  if (dns_) cudaStreamDestroy(dns_);
+  for (cudaEvent_t e : ev_pipe_) cudaEventDestroy(e);
   if (pool_) cudaFree(pool_);
   if (host_stage_) cudaFreeHost(host_stage_);
 }
@@ -484,9 +487,74 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   if (wall_s) *wall_s = static_cast<double>(ms) * 1e-3;
 }
 
+// Host-buffer step with the PCIe copies hidden behind each other and behind
+// the kernel: the slab is cut into chunks of planes; chunk c's H2D (copy
+// engine 1), the fused kernel on the output planes it completes, and the
+// D2H of those planes (copy engine 2) run on three streams linked by events.
+// The periodic halos need the first and last R planes, so those go first.
+void Team::step_host_pipelined(const void* x_in, void* x_out) {
+  if (!ups_) {
+    IMB_CUDA(cudaStreamCreateWithFlags(&ups_, cudaStreamNonBlocking));
+    IMB_CUDA(cudaStreamCreateWithFlags(&dns_, cudaStreamNonBlocking));
+  }
+  const int nch = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(8, ni_ / (8 * R_))));
+  while (ev_pipe_.size() < static_cast<std::size_t>(2 * nch + 2)) {
+    cudaEvent_t e;
+    IMB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_pipe_.push_back(e);
+  }
+  const std::size_t pb = plane_bytes();
+  const char* in = static_cast<const char*>(x_in);
+  char* out = static_cast<char*>(x_out);
+  auto xplane = [&](std::int64_t p) { return static_cast<char*>(x_) + static_cast<std::size_t>(p + R_) * pb; };
+  auto nplane = [&](std::int64_t p) { return static_cast<char*>(xn_) + static_cast<std::size_t>(p + R_) * pb; };
+  auto h2d = [&](std::int64_t a, std::int64_t b) {
+    if (b > a)
+      IMB_CUDA(cudaMemcpyAsync(xplane(a), in + static_cast<std::size_t>(a) * pb,
+                               static_cast<std::size_t>(b - a) * pb, cudaMemcpyHostToDevice, ups_));
+  };
+  cudaEvent_t ev_start = ev_pipe_[0], ev_edges = ev_pipe_[1];
+  IMB_CUDA(cudaEventRecord(ev_start, cs_));
+  IMB_CUDA(cudaStreamWaitEvent(ups_, ev_start, 0));
+  IMB_CUDA(cudaStreamWaitEvent(dns_, ev_start, 0));
+  // edges + periodic self halos
+  h2d(0, R_);
+  h2d(ni_ - R_, ni_);
+  const std::size_t hb = static_cast<std::size_t>(R_) * pb;
+  IMB_CUDA(cudaMemcpyAsync(xplane(-R_), xplane(ni_ - R_), hb, cudaMemcpyDeviceToDevice, ups_));
+  IMB_CUDA(cudaMemcpyAsync(xplane(ni_), xplane(0), hb, cudaMemcpyDeviceToDevice, ups_));
+  IMB_CUDA(cudaEventRecord(ev_edges, ups_));
+  std::int64_t done_out = 0;
+  for (int c = 0; c < nch; ++c) {
+    const std::int64_t b0 = ni_ * c / nch, b1 = ni_ * (c + 1) / nch;
+    h2d(std::max(b0, R_), std::min(b1, ni_ - R_));
+    cudaEvent_t up = ev_pipe_[2 + 2 * c], comp = ev_pipe_[3 + 2 * c];
+    IMB_CUDA(cudaEventRecord(up, ups_));
+    IMB_CUDA(cudaStreamWaitEvent(cs_, up, 0));
+    const std::int64_t o1 = (c == nch - 1) ? ni_ : std::max(done_out, b1 - R_);
+    fused_range(done_out, o1);
+    IMB_CUDA(cudaEventRecord(comp, cs_));
+    IMB_CUDA(cudaStreamWaitEvent(dns_, comp, 0));
+    if (o1 > done_out)
+      IMB_CUDA(cudaMemcpyAsync(out + static_cast<std::size_t>(done_out) * pb, nplane(done_out),
+                               static_cast<std::size_t>(o1 - done_out) * pb, cudaMemcpyDeviceToHost,
+                               dns_));
+    done_out = o1;
+  }
+  (void)ev_edges;
+  IMB_CUDA(cudaStreamSynchronize(dns_));
+  IMB_CUDA(cudaStreamSynchronize(cs_));
+  std::swap(x_, xn_);
+}
+
 void Team::step_host(const void* x_in, void* x_out) {
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
   IMB_CUDA(cudaSetDevice(device_));
+  if (!static_halo_ok_) exchange_static();
+  if (!(nccl_ && nccl_->nranks() > 1) && tmp_[0] == nullptr && ni_ >= 4 * R_) {
+    step_host_pipelined(x_in, x_out);
+    return;
+  }
   const std::size_t bytes = static_cast<std::size_t>(ni_) * plane_bytes();
   char* interior = static_cast<char*>(x_) + static_cast<std::size_t>(R_) * plane_bytes();
   IMB_CUDA(cudaMemcpyAsync(interior, x_in, bytes, cudaMemcpyHostToDevice, cs_));

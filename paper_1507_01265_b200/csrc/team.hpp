@@ -92,6 +92,9 @@ class Team {
   void compute_step();  // x (halo-complete) -> xn, then swap
   void fused_range(std::int64_t o0, std::int64_t o1);
   void step_overlapped();  // NCCL exchange hidden behind the interior planes
+  void step_host_pipelined(const void* x_in, void* x_out);
+  cudaStream_t ups_ = nullptr, dns_ = nullptr;  // H2D / D2H copy streams (step_host)
+  std::vector<cudaEvent_t> ev_pipe_;
   template <class T>
   void compute_step_t();
   void* fbuf(int field) const;

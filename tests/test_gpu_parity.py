@@ -138,6 +138,27 @@ def test_step_host_matches_run_and_reset(orc):
     assert rel_err(xout, oracle_run(orc, f, opts, 1)) <= 1e-12
 
 
+@pytest.mark.parametrize("opts,shape", [(Options(2, True, True), (96, 20, 64)),
+                                        (Options(2, False, False), (64, 7, 128)),
+                                        (Options(2, True, False), (200, 13, 32))])
+def test_pipelined_step_host_is_bit_identical(orc, opts, shape):
+    # step_host on a fused shape takes the chunked H2D / kernel / D2H pipeline;
+    # it must equal the device-resident run() bit for bit.
+    dt = np.float64 if opts.fp64 else np.float32
+    f = orc.init_fields(2, *shape, seed=31, dtype=dt)
+    with Team(*shape, opts) as t:
+        t.upload_all(*f)
+        xin = np.ascontiguousarray(f[0])
+        xout = np.empty_like(xin)
+        t.step_host(xin, xout)
+        xout2 = np.empty_like(xin)
+        t.step_host(xout, xout2)  # second step from the host result
+        t.reset()
+        t.run(2)
+        np.testing.assert_array_equal(t.download("x"), xout2)
+    assert rel_err(xout2, oracle_run(orc, f, opts, 2)) <= TOL[opts.fp64]
+
+
 def test_stage_max7_min7_on_gpu(orc):
     import ctypes as C
     n, m, l, h = 8, 9, 10, 1

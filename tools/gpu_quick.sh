@@ -1,7 +1,7 @@
 #!/bin/bash
 # Quick GPU iteration: parity tests (fused subset) + per-config step timing.
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "fused or config or group" > gpurun_out/pytest_quick.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "fused or config or group or step_host" > gpurun_out/pytest_quick.log 2>&1
 echo "pytest=$?"; tail -3 gpurun_out/pytest_quick.log
 for nt in ${NTS:-default}; do
   echo "IMB_FUSED_NT=$nt"
