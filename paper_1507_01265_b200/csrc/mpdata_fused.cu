@@ -37,6 +37,17 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+#ifdef IMB_PHASE_TIMING
+// Debug-only per-phase cycle accounting (lane 0 of every warp), off in the product build.
+__device__ unsigned long long g_phase_cycles[10];
+#define IMB_T(i) const long long imb_tp##i = clock64();
+#define IMB_ACC(slot, a, b) \
+  if (lane == 0) atomicAdd(&g_phase_cycles[slot], static_cast<unsigned long long>(imb_tp##b - imb_tp##a));
+#else
+#define IMB_T(i)
+#define IMB_ACC(slot, a, b)
+#endif
+
 template <class T, int L, int RW, int NW, int NS, bool NONOS>
 struct Cfg {
   static constexpr int KPT = L / (32 * NS);       // consecutive k per lane and segment
@@ -499,8 +510,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   const int tstart = NONOS ? ib - 2 : ib;
   for (int t = tstart; t < ie; ++t) {
     const bool emit = t >= ib;
+    IMB_T(0)
     stage_donor(t + lag);  // psi^(1) of the newest plane
+    IMB_T(1)
     __syncthreads();
+    IMB_T(2)
+    IMB_ACC(0, 0, 1)
+    IMB_ACC(1, 1, 2)
     if constexpr (NONOS) {
       const int p1 = t + 1;
       T* vA = s_v + (p1 & 1) * PL;              // y-face velocities, plane t+1
@@ -512,7 +528,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const T* buB = s_bu + ((p1 + 1) & 1) * PL;  // beta, plane t
       const T* bdB = s_bd + ((p1 + 1) & 1) * PL;
       stage_pseudo(p1, false, ufresh, vA, wA);
+      IMB_T(3)
       __syncthreads();
+      IMB_T(4)
+      IMB_ACC(2, 2, 3)
+      IMB_ACC(3, 3, 4)
       // P3: 7-point bounds and beta of plane t+1.
       {
         const T* s0 = s_x1 + slot3(t) * PL;
@@ -590,7 +610,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           vstore(bdA + so, bd);
         }
       }
+      IMB_T(5)
       __syncthreads();
+      IMB_T(6)
+      IMB_ACC(4, 4, 5)
+      IMB_ACC(5, 5, 6)
       // P4: limit plane t+1 velocities; P5: final update of plane t.
       {
         const T* s0 = s_x1 + slot3(t) * PL;
@@ -663,7 +687,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           nmn[c] = nmn_new[c];
         }
       }
+      IMB_T(7)
       __syncthreads();
+      IMB_T(8)
+      IMB_ACC(6, 6, 7)
+      IMB_ACC(7, 7, 8)
     } else {
       // Plain IORD=2: pseudo-velocities of plane t, then the final update.
       stage_pseudo(t, false, ufresh, s_v, s_w);
@@ -777,6 +805,17 @@ bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool) 
   (void)nonos;
   return iord == 2 && (l == 32 || l == 64 || l == 128) && m >= 3 && m < (1 << 20);
 }
+
+#ifdef IMB_PHASE_TIMING
+extern "C" int imb_debug_phase_cycles(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+  if (reset) {
+    unsigned long long z[10] = {};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 template <class T>
 int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
