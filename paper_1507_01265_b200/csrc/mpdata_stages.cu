@@ -1,12 +1,13 @@
 // Staged MPDATA kernels: one launch per stage group, every intermediate in
-// HBM. They are the general-purpose path (any grid, any plane range) used
-// for slab boundary planes, grids too thin for the fused streaming kernel,
-// and as the structural cross-check of the fused kernel in tests.
+// HBM. They are the general path (any IORD — config 5's IORD=3 — and any
+// plane extent l), and the structural cross-check of the fused kernel.
 //
 // Device layout of every field (a "padded slab"): planes p in [0, ni + 2R),
 // local i = p - R, each plane m*l values with k contiguous — the interior
 // order of GridField::index (workload.hpp:40-43) with halos only along the
-// slab axis. j and k are periodic and wrap by index arithmetic.
+// slab axis. j and k are periodic and wrap by index arithmetic. The per-cell
+// arithmetic is the fused kernel's (mpdata_math.cuh): exact select forms,
+// one reciprocal per pseudo-velocity and per beta pair.
 #include <cuda_runtime.h>
 
 #include "mpdata_kernels.cuh"
@@ -16,28 +17,30 @@ namespace imb::dev {
 
 namespace {
 
+// A cell of the launch span: plane base offset (64-bit) and in-plane offsets
+// of the cell and its periodic j/k neighbours (32-bit).
 struct Cell {
-  std::int64_t p, j, k, jm, jp, km, kp;
+  long long base;  // p * plane
+  long long plane;
+  int o, ojm, ojp, okm, okp;
 };
 
 __device__ __forceinline__ bool locate(const Span& s, Cell& c) {
-  const std::int64_t t = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const std::int64_t plane = s.m * s.l;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int m = static_cast<int>(s.m), l = static_cast<int>(s.l);
+  const long long plane = static_cast<long long>(m) * l;
   if (t >= (s.p1 - s.p0) * plane) return false;
-  c.p = s.p0 + t / plane;
-  const std::int64_t r = t % plane;
-  c.j = r / s.l;
-  c.k = r % s.l;
-  c.jm = c.j == 0 ? s.m - 1 : c.j - 1;
-  c.jp = c.j == s.m - 1 ? 0 : c.j + 1;
-  c.km = c.k == 0 ? s.l - 1 : c.k - 1;
-  c.kp = c.k == s.l - 1 ? 0 : c.k + 1;
+  const long long p = s.p0 + t / plane;
+  const int r = static_cast<int>(t - (p - s.p0) * plane);
+  const int j = r / l, k = r - j * l;
+  c.base = p * plane;
+  c.plane = plane;
+  c.o = r;
+  c.ojm = (j == 0 ? r + (m - 1) * l : r - l);
+  c.ojp = (j == m - 1 ? r - (m - 1) * l : r + l);
+  c.okm = (k == 0 ? r + l - 1 : r - 1);
+  c.okp = (k == l - 1 ? r - (l - 1) : r + 1);
   return true;
-}
-
-__device__ __forceinline__ std::int64_t at(const Span& s, std::int64_t p, std::int64_t j,
-                                           std::int64_t k) {
-  return (p * s.m + j) * s.l + k;
 }
 
 // out = x - div F(x, (U,V,W)) / h   (donor cell, and every corrective update)
@@ -49,18 +52,19 @@ __global__ void __launch_bounds__(256) k_update(Span s, const T* __restrict__ x,
                                                 const T* __restrict__ h, T* __restrict__ out) {
   Cell c;
   if (!locate(s, c)) return;
-  const std::int64_t o = at(s, c.p, c.j, c.k);
-  const T xc = x[o];
-  const std::int64_t ox = at(s, c.p + 1, c.j, c.k), oy = at(s, c.p, c.jp, c.k),
-                     oz = at(s, c.p, c.j, c.kp);
-  const T fxl = flux(x[at(s, c.p - 1, c.j, c.k)], xc, U[o]);
-  const T fxr = flux(xc, x[ox], U[ox]);
-  const T fyl = flux(x[at(s, c.p, c.jm, c.k)], xc, V[o]);
-  const T fyr = flux(xc, x[oy], V[oy]);
-  const T fzl = flux(x[at(s, c.p, c.j, c.km)], xc, W[o]);
-  const T fzr = flux(xc, x[oz], W[oz]);
+  const T* X = x + c.base;
+  const T* Ub = U + c.base;
+  const T* Vb = V + c.base;
+  const T* Wb = W + c.base;
+  const T xc = X[c.o];
+  const T fxl = upflux(X[c.o - c.plane], xc, Ub[c.o]);
+  const T fxr = upflux(xc, X[c.o + c.plane], Ub[c.o + c.plane]);
+  const T fyl = upflux(X[c.ojm], xc, Vb[c.o]);
+  const T fyr = upflux(xc, X[c.ojp], Vb[c.ojp]);
+  const T fzl = upflux(X[c.okm], xc, Wb[c.o]);
+  const T fzr = upflux(xc, X[c.okp], Wb[c.okp]);
   const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-  out[o] = xc - div / h[o];
+  out[c.base + c.o] = xc - qdiv(div, h[c.base + c.o]);
 }
 
 // Antidiffusive pseudo-velocities on all three face families.
@@ -73,49 +77,45 @@ __global__ void __launch_bounds__(256) k_pseudo(Span s, const T* __restrict__ x,
                                                 T* __restrict__ vt, T* __restrict__ wt) {
   Cell c;
   if (!locate(s, c)) return;
-  const std::int64_t p = c.p, j = c.j, k = c.k, pm = p - 1, pp = p + 1;
-  const std::int64_t o = at(s, p, j, k);
-  auto ax = [&](std::int64_t a, std::int64_t b, std::int64_t d) { return fabs(x[at(s, a, b, d)]); };
-  const T ac = fabs(x[o]);
-  const T hc = h[o];
+  const long long P = c.plane;
+  const T* X = x + c.base;  // plane p; X - P is p-1, X + P is p+1
+  const T* Ub = U + c.base;
+  const T* Vb = V + c.base;
+  const T* Wb = W + c.base;
+  const T* Hb = h + c.base;
+  const int o = c.o;
+  // in-plane offsets of the diagonal neighbours
+  const int ojmkp = c.ojm + (c.okp - o), ojmkm = c.ojm + (c.okm - o);
+  const int ojpkm = c.ojp + (c.okm - o);
+  auto A = [&](long long off) { return fabs(X[off]); };
+  const T ac = A(o);
+  const T hc = Hb[o];
   {  // x-face (i-1/2)
-    const T Un = U[o];
-    const T hb = T(0.5) * (h[at(s, pm, j, k)] + hc);
-    const T A = ratio(ac, ax(pm, j, k));
-    const T B = ratio(ax(pm, c.jp, k) + ax(p, c.jp, k), ax(pm, c.jm, k) + ax(p, c.jm, k));
-    const T C = ratio(ax(pm, j, c.kp) + ax(p, j, c.kp), ax(pm, j, c.km) + ax(p, j, c.km));
-    const T Vs = (V[at(s, pm, j, k)] + V[o]) + (V[at(s, pm, c.jp, k)] + V[at(s, p, c.jp, k)]);
-    const T Ws = (W[at(s, pm, j, k)] + W[o]) + (W[at(s, pm, j, c.kp)] + W[at(s, p, j, c.kp)]);
-    ut[o] = pseudo(Un, hb, A, Vs, B, Ws, C);
+    const T Vs = (Vb[o - P] + Vb[o]) + (Vb[c.ojp - P] + Vb[c.ojp]);
+    const T Ws = (Wb[o - P] + Wb[o]) + (Wb[c.okp - P] + Wb[c.okp]);
+    ut[c.base + o] = pseudo_face<T>(Ub[o], Hb[o - P], hc, ac, A(o - P), A(c.ojp - P) + A(c.ojp),
+                                    A(c.ojm - P) + A(c.ojm), Vs, A(c.okp - P) + A(c.okp),
+                                    A(c.okm - P) + A(c.okm), Ws);
   }
   {  // y-face (j-1/2)
-    const T Vn = V[o];
-    const T hb = T(0.5) * (h[at(s, p, c.jm, k)] + hc);
-    const T A = ratio(ac, ax(p, c.jm, k));
-    const T B = ratio(ax(pp, c.jm, k) + ax(pp, j, k), ax(pm, c.jm, k) + ax(pm, j, k));
-    const T C = ratio(ax(p, c.jm, c.kp) + ax(p, j, c.kp), ax(p, c.jm, c.km) + ax(p, j, c.km));
-    const T Us = (U[at(s, p, c.jm, k)] + U[o]) + (U[at(s, pp, c.jm, k)] + U[at(s, pp, j, k)]);
-    const T Ws = (W[at(s, p, c.jm, k)] + W[o]) + (W[at(s, p, c.jm, c.kp)] + W[at(s, p, j, c.kp)]);
-    vt[o] = pseudo(Vn, hb, A, Us, B, Ws, C);
+    const T Us = (Ub[c.ojm] + Ub[o]) + (Ub[c.ojm + P] + Ub[o + P]);
+    const T Ws = (Wb[c.ojm] + Wb[o]) + (Wb[ojmkp] + Wb[c.okp]);
+    vt[c.base + o] = pseudo_face<T>(Vb[o], Hb[c.ojm], hc, ac, A(c.ojm), A(c.ojm + P) + A(o + P),
+                                    A(c.ojm - P) + A(o - P), Us, A(ojmkp) + A(c.okp),
+                                    A(ojmkm) + A(c.okm), Ws);
   }
   {  // z-face (k-1/2)
-    const T Wn = W[o];
-    const T hb = T(0.5) * (h[at(s, p, j, c.km)] + hc);
-    const T A = ratio(ac, ax(p, j, c.km));
-    const T B = ratio(ax(pp, j, c.km) + ax(pp, j, k), ax(pm, j, c.km) + ax(pm, j, k));
-    const T C = ratio(ax(p, c.jp, c.km) + ax(p, c.jp, k), ax(p, c.jm, c.km) + ax(p, c.jm, k));
-    const T Us = (U[at(s, p, j, c.km)] + U[o]) + (U[at(s, pp, j, c.km)] + U[at(s, pp, j, k)]);
-    const T Vs = (V[at(s, p, j, c.km)] + V[o]) + (V[at(s, p, c.jp, c.km)] + V[at(s, p, c.jp, k)]);
-    wt[o] = pseudo(Wn, hb, A, Us, B, Vs, C);
+    const T Us = (Ub[c.okm] + Ub[o]) + (Ub[c.okm + P] + Ub[o + P]);
+    const T Vs = (Vb[c.okm] + Vb[o]) + (Vb[ojpkm] + Vb[c.ojp]);
+    wt[c.base + o] = pseudo_face<T>(Wb[o], Hb[c.okm], hc, ac, A(c.okm), A(c.okm + P) + A(o + P),
+                                    A(c.okm - P) + A(o - P), Us, A(ojpkm) + A(c.ojp),
+                                    A(ojmkm) + A(c.ojm), Vs);
   }
 }
 
 template <class T>
-__device__ __forceinline__ void ext7(const Span& s, const T* __restrict__ x, const Cell& c,
-                                     T& hi, T& lo) {
-  const T v[7] = {x[at(s, c.p, c.j, c.k)],  x[at(s, c.p - 1, c.j, c.k)], x[at(s, c.p + 1, c.j, c.k)],
-                  x[at(s, c.p, c.jm, c.k)], x[at(s, c.p, c.jp, c.k)],    x[at(s, c.p, c.j, c.km)],
-                  x[at(s, c.p, c.j, c.kp)]};
+__device__ __forceinline__ void ext7(const T* X, long long P, const Cell& c, T& hi, T& lo) {
+  const T v[7] = {X[c.o], X[c.o - P], X[c.o + P], X[c.ojm], X[c.ojp], X[c.okm], X[c.okp]};
   hi = v[0];
   lo = v[0];
 #pragma unroll
@@ -132,12 +132,12 @@ __global__ void __launch_bounds__(256) k_bounds(Span s, const T* __restrict__ x,
                                                 T* __restrict__ mx, T* __restrict__ mn) {
   Cell c;
   if (!locate(s, c)) return;
-  const std::int64_t o = at(s, c.p, c.j, c.k);
+  const long long o = c.base + c.o;
   T hi, lo;
-  ext7(s, x, c, hi, lo);
+  ext7(x + c.base, c.plane, c, hi, lo);
   if (first) {
     T h2, l2;
-    ext7(s, xn, c, h2, l2);
+    ext7(xn + c.base, c.plane, c, h2, l2);
     hi = tmax(hi, h2);
     lo = tmin(lo, l2);
   } else {
@@ -159,21 +159,35 @@ __global__ void __launch_bounds__(256) k_beta(Span s, const T* __restrict__ x,
                                               T* __restrict__ bd) {
   Cell c;
   if (!locate(s, c)) return;
-  const std::int64_t o = at(s, c.p, c.j, c.k);
-  const std::int64_t ox = at(s, c.p + 1, c.j, c.k), oy = at(s, c.p, c.jp, c.k),
-                     oz = at(s, c.p, c.j, c.kp);
-  const T xc = x[o];
-  const T axl = flux(x[at(s, c.p - 1, c.j, c.k)], xc, ut[o]);
-  const T axr = flux(xc, x[ox], ut[ox]);
-  const T ayl = flux(x[at(s, c.p, c.jm, c.k)], xc, vt[o]);
-  const T ayr = flux(xc, x[oy], vt[oy]);
-  const T azl = flux(x[at(s, c.p, c.j, c.km)], xc, wt[o]);
-  const T azr = flux(xc, x[oz], wt[oz]);
-  const T fin = ((pos(axl) - neg(axr)) + (pos(ayl) - neg(ayr))) + (pos(azl) - neg(azr));
-  const T fout = ((pos(axr) - neg(axl)) + (pos(ayr) - neg(ayl))) + (pos(azr) - neg(azl));
-  const T hc = h[o];
-  bu[o] = ((mx[o] - xc) * hc) / (fin + Eps<T>::value);
-  bd[o] = ((xc - mn[o]) * hc) / (fout + Eps<T>::value);
+  const long long P = c.plane;
+  const T* X = x + c.base;
+  const T* Ut = ut + c.base;
+  const T* Vt = vt + c.base;
+  const T* Wt = wt + c.base;
+  const int o = c.o;
+  const T xc = X[o];
+  const T axl = upflux(X[o - P], xc, Ut[o]);
+  const T axr = upflux(xc, X[o + P], Ut[o + P]);
+  const T ayl = upflux(X[c.ojm], xc, Vt[o]);
+  const T ayr = upflux(xc, X[c.ojp], Vt[c.ojp]);
+  const T azl = upflux(X[c.okm], xc, Wt[o]);
+  const T azr = upflux(xc, X[c.okp], Wt[c.okp]);
+  // 2*pos(f) = f + |f|, -2*neg(f) = |f| - f: exact, so these are 2*fin, 2*fout.
+  const T fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) + ((ayl + fabs(ayl)) + (fabs(ayr) - ayr))) +
+                 ((azl + fabs(azl)) + (fabs(azr) - azr));
+  const T fout2 = (((axr + fabs(axr)) + (fabs(axl) - axl)) + ((ayr + fabs(ayr)) + (fabs(ayl) - ayl))) +
+                  ((azr + fabs(azr)) + (fabs(azl) - azl));
+  const long long g = c.base + o;
+  const T hc = h[g];
+  const T di = T(0.5) * fin2 + Eps<T>::value, dou = T(0.5) * fout2 + Eps<T>::value;
+  if constexpr (sizeof(T) == 8) {
+    const T r = rcp(di * dou);
+    bu[g] = ((mx[g] - xc) * hc) * dou * r;
+    bd[g] = ((xc - mn[g]) * hc) * di * r;
+  } else {
+    bu[g] = qdiv((mx[g] - xc) * hc, di);
+    bd[g] = qdiv((xc - mn[g]) * hc, dou);
+  }
 }
 
 // Limit the pseudo-velocities in place.
@@ -183,14 +197,15 @@ __global__ void __launch_bounds__(256) k_limit(Span s, T* __restrict__ ut, T* __
                                                const T* __restrict__ bd) {
   Cell c;
   if (!locate(s, c)) return;
-  const std::int64_t o = at(s, c.p, c.j, c.k);
-  const T buc = bu[o], bdc = bd[o];
-  std::int64_t L = at(s, c.p - 1, c.j, c.k);
-  ut[o] = limit(ut[o], bd[L], buc, bu[L], bdc);
-  L = at(s, c.p, c.jm, c.k);
-  vt[o] = limit(vt[o], bd[L], buc, bu[L], bdc);
-  L = at(s, c.p, c.j, c.km);
-  wt[o] = limit(wt[o], bd[L], buc, bu[L], bdc);
+  const long long P = c.plane;
+  const T* Bu = bu + c.base;
+  const T* Bd = bd + c.base;
+  const int o = c.o;
+  const long long g = c.base + o;
+  const T buc = Bu[o], bdc = Bd[o];
+  ut[g] = limit_sel(ut[g], Bd[o - P], buc, Bu[o - P], bdc);
+  vt[g] = limit_sel(vt[g], Bd[c.ojm], buc, Bu[c.ojm], bdc);
+  wt[g] = limit_sel(wt[g], Bd[c.okm], buc, Bu[c.okm], bdc);
 }
 
 unsigned blocks_for(const Span& s) {
