@@ -222,6 +222,41 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
   // cell group c = (row rr, segment sg): first k of this lane in the segment
   auto k0of = [&](int c) { return (c % NS) * 32 * K + lane * K; };
+  // Point-to-point phase synchronisation between neighbouring warps instead
+  // of block barriers: every cross-warp dependency of a phase is on the rows
+  // of warps w-1 and w+1 (j +- 1), and every shared slot a warp overwrites was
+  // last read by those warps one phase earlier. So a warp may start phase ph
+  // once both neighbours have finished phase ph-1; warps then drift apart
+  // along the row chain and overlap one another's load latency.
+  __shared__ volatile int prog[NW];
+  int phase = 0;  // phases completed by this warp
+  auto publish = [&](int ph) {
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      prog[warp] = ph;
+    }
+  };
+  auto await = [&](int ph) {
+    if (lane == 0) {
+      if (warp > 0)
+        while (prog[warp - 1] < ph - 1) {}
+      if (warp < NW - 1)
+        while (prog[warp + 1] < ph - 1) {}
+      __threadfence_block();
+    }
+    __syncwarp();
+  };
+  // close the phase this warp just ran and wait until the next may start
+  auto nb_sync = [&]() {
+#ifdef IMB_P2P_SYNC
+    ++phase;
+    publish(phase);
+    await(phase + 1);
+#else
+    __syncthreads();
+#endif
+  };
   // neighbour helpers: G = global source row, S = shared source row
 #define KMG(vec, row, k0) kminus<L, NS, true>(vec, row, k0, lane)
 #define KPG(vec, row, k0) kplus<L, NS, true>(vec, row, k0, lane)
@@ -442,8 +477,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       nmn[c] = nmn_new[c];
     }
   }
+  if (lane == 0) prog[warp] = 0;
   __syncthreads();
   stage_pseudo(ib - lag, true, ucar, nullptr, nullptr);
+  phase = 1;  // the warm-up pseudo is phase 1
+  publish(phase);
 
   const int tstart = NONOS ? ib - 2 : ib;
   for (int t = tstart; t < ie; ++t) {
@@ -451,7 +489,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     IMB_T(0)
     stage_donor(t + lag);  // psi^(1) of the newest plane
     IMB_T(1)
-    __syncthreads();
+    nb_sync();
     IMB_T(2)
     IMB_ACC(0, 0, 1)
     IMB_ACC(1, 1, 2)
@@ -467,7 +505,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const T* bdB = s_bd + ((p1 + 1) & 1) * PL;
       stage_pseudo(p1, false, ufresh, vA, wA);
       IMB_T(3)
-      __syncthreads();
+      nb_sync();
       IMB_T(4)
       IMB_ACC(2, 2, 3)
       IMB_ACC(3, 3, 4)
@@ -549,7 +587,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       IMB_T(5)
-      __syncthreads();
+      nb_sync();
       IMB_T(6)
       IMB_ACC(4, 4, 5)
       IMB_ACC(5, 5, 6)
@@ -626,14 +664,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       IMB_T(7)
-      __syncthreads();
+      nb_sync();
       IMB_T(8)
       IMB_ACC(6, 6, 7)
       IMB_ACC(7, 7, 8)
     } else {
       // Plain IORD=2: pseudo-velocities of plane t, then the final update.
       stage_pseudo(t, false, ufresh, s_v, s_w);
-      __syncthreads();
+      nb_sync();
       const T* sm1 = s_x1 + slot3(t - 1) * PL;
       const T* s0 = s_x1 + slot3(t) * PL;
       const T* s1 = s_x1 + slot3(t + 1) * PL;
@@ -670,7 +708,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         if (j < m) vstore(O + gj[rr] + k0, res);
         ucar[c] = ufresh[c];
       }
-      __syncthreads();
+      nb_sync();
     }
   }
 #undef KMG
@@ -729,8 +767,25 @@ int dispatch_l(const FusedShape& fs, const T* x, const T* u, const T* v, const T
   // psi^n star; fp32 holds 4 floats per lane and carries the star.
   constexpr bool D = sizeof(T) == 8;
   switch (fs.l) {
-    case 128:
+    case 128: {
+#ifdef IMB_FUSED_VARIANTS
+      // Experiment hook: IMB_FUSED_VARIANT=<NS><STARC>, e.g. 21 = NS 2 with the star carry.
+      static const int var = [] {
+        const char* e = std::getenv("IMB_FUSED_VARIANT");
+        return e ? std::atoi(e) : 0;
+      }();
+      switch (var) {
+        case 10: return launch_cfg<T, 128, 1, 16, 1, NONOS, false>(fs, x, u, v, w, h, out, num_sms, st);
+        case 11: return launch_cfg<T, 128, 1, 16, 1, NONOS, true>(fs, x, u, v, w, h, out, num_sms, st);
+        case 20: return launch_cfg<T, 128, 1, 16, 2, NONOS, false>(fs, x, u, v, w, h, out, num_sms, st);
+        case 21: return launch_cfg<T, 128, 1, 16, 2, NONOS, true>(fs, x, u, v, w, h, out, num_sms, st);
+        case 40: return launch_cfg<T, 128, 1, 16, 4, NONOS, false>(fs, x, u, v, w, h, out, num_sms, st);
+        case 41: return launch_cfg<T, 128, 1, 16, 4, NONOS, true>(fs, x, u, v, w, h, out, num_sms, st);
+        default: break;
+      }
+#endif
       return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
+    }
     case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
     case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
     default: return 0;
