@@ -75,6 +75,12 @@ struct Args {
   int nseg;         // i segments
   int o0, o1;       // output plane range (interior coordinates)
   long long plane;  // m * l
+  // IORD=3 split (MODE 1 writes, MODE 2 reads): bounds and limited velocities
+  T* mxo;
+  T* mno;
+  T* uo;
+  T* vo;
+  T* wo;
 };
 
 // ---- per-lane vectors of K consecutive k values ---------------------------
@@ -184,7 +190,11 @@ __device__ __forceinline__ Vec<T, K> vabs(const Vec<T, K>& a) {
   return r;
 }
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC>
+// MODE 0: one IORD=2 step. MODE 1: donor + first corrective pass of an
+// IORD=3 step, additionally writing the pass's limited velocities and 7-point
+// bounds. MODE 2: the second corrective pass from psi^(2) (read instead of the
+// donor), the limited velocities (as u, v, w) and the accumulated bounds.
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   using C = Cfg<T, L, RW, NW, NS, NONOS>;
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS;
@@ -222,41 +232,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
   // cell group c = (row rr, segment sg): first k of this lane in the segment
   auto k0of = [&](int c) { return (c % NS) * 32 * K + lane * K; };
-  // Point-to-point phase synchronisation between neighbouring warps instead
-  // of block barriers: every cross-warp dependency of a phase is on the rows
-  // of warps w-1 and w+1 (j +- 1), and every shared slot a warp overwrites was
-  // last read by those warps one phase earlier. So a warp may start phase ph
-  // once both neighbours have finished phase ph-1; warps then drift apart
-  // along the row chain and overlap one another's load latency.
-  __shared__ volatile int prog[NW];
-  int phase = 0;  // phases completed by this warp
-  auto publish = [&](int ph) {
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      prog[warp] = ph;
-    }
+  // MODE 1: plane t+1 values of an own tile row are stored once (segments
+  // abut: this block owns planes [ib, ie), the last segment also plane o1).
+  auto keep = [&](int t, int r) {
+    const int p = t + 1;
+    return p >= ib && (p < ie || ie == a.o1) && r >= C::HALO && r < RR - C::HALO &&
+           j0 + r - C::HALO < m;
   };
-  auto await = [&](int ph) {
-    if (lane == 0) {
-      if (warp > 0)
-        while (prog[warp - 1] < ph - 1) {}
-      if (warp < NW - 1)
-        while (prog[warp + 1] < ph - 1) {}
-      __threadfence_block();
-    }
-    __syncwarp();
-  };
-  // close the phase this warp just ran and wait until the next may start
-  auto nb_sync = [&]() {
-#ifdef IMB_P2P_SYNC
-    ++phase;
-    publish(phase);
-    await(phase + 1);
-#else
-    __syncthreads();
-#endif
-  };
+  // Phase barrier. (A point-to-point variant — each warp waiting only for its
+  // j-neighbour warps through shared-memory progress counters — was measured
+  // 3-4x slower than the hardware barrier and removed.)
+  auto nb_sync = [&]() { __syncthreads(); };
   // neighbour helpers: G = global source row, S = shared source row
 #define KMG(vec, row, k0) kminus<L, NS, true>(vec, row, k0, lane)
 #define KPG(vec, row, k0) kplus<L, NS, true>(vec, row, k0, lane)
@@ -276,6 +262,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     const T* W = a.w + pl(p);
     const T* H = a.h + pl(p);
     T* dst = s_x1 + slot3(p) * PL;
+    if constexpr (MODE == 2) {  // psi^(2) is an input: stage it, carry the bounds
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int rr = c / NS, k0 = k0of(c);
+        const int g = gj[rr] + k0;
+        vstore(dst + (warp * RW + rr) * L + k0, vload<T, K>(X + g));
+        if constexpr (STARC) {
+          nmx_new[c] = vload<T, K>(a.mxo + pl(p) + g);
+          nmn_new[c] = vload<T, K>(a.mno + pl(p) + g);
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int rr = c / NS, k0 = k0of(c);
@@ -477,11 +476,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       nmn[c] = nmn_new[c];
     }
   }
-  if (lane == 0) prog[warp] = 0;
   __syncthreads();
   stage_pseudo(ib - lag, true, ucar, nullptr, nullptr);
-  phase = 1;  // the warm-up pseudo is phase 1
-  publish(phase);
 
   const int tstart = NONOS ? ib - 2 : ib;
   for (int t = tstart; t < ie; ++t) {
@@ -532,6 +528,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if constexpr (STARC) {
             mx = nmx[c];
             mn = nmn[c];
+          } else if constexpr (MODE == 2) {  // bounds of the previous pass
+            const int g = gj[rr] + k0;
+            mx = vload<T, K>(a.mxo + pl(p1) + g);
+            mn = vload<T, K>(a.mno + pl(p1) + g);
           } else {  // psi^n star of plane t+1, reloaded
             const int g = gj[rr] + k0;
             const V nc = vload<T, K>(Xn1 + g);
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const V wa = sload<T, K>(wA + so);
           const V wap = KPS(wa, wA + r * L, k0);
           const V hc = vload<T, K>(H1 + gj[rr] + k0);
-          V bu, bd;
+          V bu, bd, his, los;
 #pragma unroll
           for (int e = 0; e < K; ++e) {
             const T x0 = xc.e[e];
@@ -558,6 +558,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
                               tmax(tmax(ym.e[e], yp.e[e]), tmax(zm.e[e], zp.e[e])));
             const T lo = tmin(tmin(tmin(mn.e[e], x0), tmin(xm.e[e], xp.e[e])),
                               tmin(tmin(ym.e[e], yp.e[e]), tmin(zm.e[e], zp.e[e])));
+            his.e[e] = hi;
+            los.e[e] = lo;
             const T axl = upflux(xm.e[e], x0, ucar[c].e[e]);
             const T axr = upflux(x0, xp.e[e], ufresh[c].e[e]);
             const T ayl = upflux(ym.e[e], x0, va.e[e]);
@@ -584,6 +586,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
           vstore(buA + so, bu);
           vstore(bdA + so, bd);
+          if constexpr (MODE == 1) {  // bounds for the next pass
+            if (keep(t, r)) {
+              vstore(a.mxo + pl(p1) + gj[rr] + k0, his);
+              vstore(a.mno + pl(p1) + gj[rr] + k0, los);
+            }
+          }
         }
       }
       IMB_T(5)
@@ -612,6 +620,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             for (int e = 0; e < K; ++e)
               res.e[e] = limit_sel(va.e[e], bdm.e[e], bu.e[e], bum.e[e], bd.e[e]);
             vstore(vA + so, res);
+            if constexpr (MODE == 1) {
+              if (keep(t, r)) vstore(a.vo + pl(p1) + gj[rr] + k0, res);
+            }
           }
           if (r >= RR - 2) continue;
           V fxr;
@@ -621,14 +632,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const V buo = sload<T, K>(buB + so), bdo = sload<T, K>(bdB + so);
             const V xc = sload<T, K>(s0 + so);
             const V x1 = sload<T, K>(s1 + so);
-            V wres;
+            V wres, uls;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
               wres.e[e] = limit_sel(wa.e[e], bdkm.e[e], bu.e[e], bukm.e[e], bd.e[e]);
               const T ul = limit_sel(ucar[c].e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
+              uls.e[e] = ul;
               fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
             }
             vstore(wA + so, wres);
+            if constexpr (MODE == 1) {
+              if (keep(t, r)) {
+                vstore(a.wo + pl(p1) + gj[rr] + k0, wres);
+                vstore(a.uo + pl(p1) + gj[rr] + k0, uls);
+              }
+            }
           }
           if (emit) {
             const V xc = sload<T, K>(s0 + so);
@@ -739,55 +757,41 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   return best;
 }
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC>
-int launch_cfg(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
-               T* out, int num_sms, cudaStream_t st) {
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE>
+int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
   using C = Cfg<T, L, RW, NW, NS, NONOS>;
+  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
-    cudaFuncSetAttribute(k_fused<T, L, RW, NW, NS, NONOS, STARC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T, L, RW, NW, NS, NONOS, STARC>, C::NT,
-                                                  C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, C::SMEM);
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
   const Plan p = plan_grid(fs.m, C::TJ, fs.o1 - fs.o0, per_sm * num_sms, NONOS ? 4 : 2);
-  Args<T> a{x, u, v, w, h, out, static_cast<int>(fs.m), static_cast<int>(fs.R), p.ntj, p.nseg,
-            static_cast<int>(fs.o0), static_cast<int>(fs.o1), fs.m * fs.l};
-  k_fused<T, L, RW, NW, NS, NONOS, STARC><<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
+  Args<T> a = proto;
+  a.m = static_cast<int>(fs.m);
+  a.R = static_cast<int>(fs.R);
+  a.ntj = p.ntj;
+  a.nseg = p.nseg;
+  a.o0 = static_cast<int>(fs.o0);
+  a.o1 = static_cast<int>(fs.o1);
+  a.plane = fs.m * fs.l;
+  kern<<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
   return 1;
 }
 
-template <class T, bool NONOS>
-int dispatch_l(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w, const T* h,
-               T* out, int num_sms, cudaStream_t st) {
+template <class T, bool NONOS, int MODE>
+int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t st) {
   // fp64 keeps lane vectors at 2 doubles (register budget) and reloads the
   // psi^n star; fp32 holds 4 floats per lane and carries the star.
   constexpr bool D = sizeof(T) == 8;
   switch (fs.l) {
-    case 128: {
-#ifdef IMB_FUSED_VARIANTS
-      // Experiment hook: IMB_FUSED_VARIANT=<NS><STARC>, e.g. 21 = NS 2 with the star carry.
-      static const int var = [] {
-        const char* e = std::getenv("IMB_FUSED_VARIANT");
-        return e ? std::atoi(e) : 0;
-      }();
-      switch (var) {
-        case 10: return launch_cfg<T, 128, 1, 16, 1, NONOS, false>(fs, x, u, v, w, h, out, num_sms, st);
-        case 11: return launch_cfg<T, 128, 1, 16, 1, NONOS, true>(fs, x, u, v, w, h, out, num_sms, st);
-        case 20: return launch_cfg<T, 128, 1, 16, 2, NONOS, false>(fs, x, u, v, w, h, out, num_sms, st);
-        case 21: return launch_cfg<T, 128, 1, 16, 2, NONOS, true>(fs, x, u, v, w, h, out, num_sms, st);
-        case 40: return launch_cfg<T, 128, 1, 16, 4, NONOS, false>(fs, x, u, v, w, h, out, num_sms, st);
-        case 41: return launch_cfg<T, 128, 1, 16, 4, NONOS, true>(fs, x, u, v, w, h, out, num_sms, st);
-        default: break;
-      }
-#endif
-      return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
-    }
-    case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
-    case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D>(fs, x, u, v, w, h, out, num_sms, st);
+    case 128: return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+    case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+    case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     default: return 0;
   }
 }
@@ -795,8 +799,8 @@ int dispatch_l(const FusedShape& fs, const T* x, const T* u, const T* v, const T
 }  // namespace
 
 bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool) {
-  (void)nonos;
-  return iord == 2 && (l == 32 || l == 64 || l == 128) && m >= 3 && m < (1 << 20);
+  const bool shape = (l == 32 || l == 64 || l == 128) && m >= 3 && m < (1 << 20);
+  return shape && (iord == 2 || (iord == 3 && nonos));
 }
 
 #ifdef IMB_PHASE_TIMING
@@ -814,14 +818,38 @@ template <class T>
 int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
                  const T* w, const T* h, T* out, int num_sms, cudaStream_t st) {
   if (iord != 2) return 0;
-  return nonos ? dispatch_l<T, true>(fs, x, u, v, w, h, out, num_sms, st)
-               : dispatch_l<T, false>(fs, x, u, v, w, h, out, num_sms, st);
+  Args<T> a{x, u, v, w, h, out, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+  return nonos ? dispatch_l<T, true, 0>(fs, a, num_sms, st)
+               : dispatch_l<T, false, 0>(fs, a, num_sms, st);
 }
+
+template <class T>
+int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w,
+                  const T* h, T* x2, T* mx, T* mn, T* u2, T* v2, T* w2, T* out, int num_sms,
+                  cudaStream_t st) {
+  // pass 2 (with the donor) over the output planes widened by the radius of
+  // the limited pass 3 (2), then pass 3 on the requested planes.
+  FusedShape f1 = fs;
+  f1.o0 = fs.o0 - 2;
+  f1.o1 = fs.o1 + 2;
+  Args<T> a1{x, u, v, w, h, x2, 0, 0, 0, 0, 0, 0, 0, mx, mn, u2, v2, w2};
+  int n = dispatch_l<T, true, 1>(f1, a1, num_sms, st);
+  Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr};
+  n += dispatch_l<T, true, 2>(fs, a2, num_sms, st);
+  return n;
+}
+
 template int launch_fused<double>(const FusedShape&, int, int, const double*, const double*,
                                   const double*, const double*, const double*, double*, int,
                                   cudaStream_t);
 template int launch_fused<float>(const FusedShape&, int, int, const float*, const float*,
                                  const float*, const float*, const float*, float*, int,
                                  cudaStream_t);
+template int launch_fused3<double>(const FusedShape&, const double*, const double*, const double*,
+                                   const double*, const double*, double*, double*, double*,
+                                   double*, double*, double*, double*, int, cudaStream_t);
+template int launch_fused3<float>(const FusedShape&, const float*, const float*, const float*,
+                                  const float*, const float*, float*, float*, float*, float*,
+                                  float*, float*, float*, int, cudaStream_t);
 
 }  // namespace imb::dev

@@ -53,5 +53,11 @@ bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool f
 template <class T>
 int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
                  const T* w, const T* h, T* out, int num_sms, cudaStream_t st);
+// IORD=3 + limiter as two fused launches: donor + pass 2 (writing psi^(2),
+// its limited velocities and bounds on planes widened by 2), then pass 3.
+template <class T>
+int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w,
+                  const T* h, T* x2, T* mx, T* mn, T* u2, T* v2, T* w2, T* out, int num_sms,
+                  cudaStream_t st);
 
 }  // namespace imb::dev

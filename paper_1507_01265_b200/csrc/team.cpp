@@ -151,10 +151,12 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
   IMB_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
   IMB_CUDA(cudaEventCreateWithFlags(&ev_static_, cudaEventDisableTiming));
   const std::size_t fbytes = static_cast<std::size_t>(P_) * plane_bytes();
-  const bool fused = dev::fused_supported(opt_.iord, opt_.nonos, m_, l_, opt_.fp64) &&
-                     ni_ >= 2 * R_;
+  // The fused kernels take any slab >= R planes (they read R halo planes);
+  // every slab of a decomposition then runs the same arithmetic.
+  const bool fused = dev::fused_supported(opt_.iord, opt_.nonos, m_, l_, opt_.fp64);
   const int ntmp = fused ? 0 : 12;
-  const std::size_t total = fbytes * static_cast<std::size_t>(7 + ntmp);
+  const int next = (fused && opt_.iord == 3) ? 6 : 0;  // psi^(2), bounds, limited velocities
+  const std::size_t total = fbytes * static_cast<std::size_t>(7 + ntmp + next);
   if (cudaMalloc(&pool_, total) != cudaSuccess) {
     cudaGetLastError();
     throw ConfigError("cannot allocate " + std::to_string(total >> 20) + " MiB on device " +
@@ -167,6 +169,7 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
   x0_ = p + 2 * fbytes;
   for (int f = 0; f < 4; ++f) st_[f] = p + static_cast<std::size_t>(3 + f) * fbytes;
   for (int t = 0; t < ntmp; ++t) tmp_[t] = p + static_cast<std::size_t>(7 + t) * fbytes;
+  for (int t = 0; t < next; ++t) ext_[t] = p + static_cast<std::size_t>(7 + ntmp + t) * fbytes;
   IMB_CUDA(cudaStreamSynchronize(cs_));
 }
 
@@ -337,7 +340,13 @@ void Team::compute_step_t() {
   T* out = static_cast<T*>(xn_);
   if (tmp_[0] == nullptr) {
     dev::FusedShape fs{m_, l_, ni_, R_, 0, ni_};
-    launches_ += dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h, out, num_sms_, cs_);
+    if (opt_.iord == 3)
+      launches_ += dev::launch_fused3<T>(
+          fs, x, u, v, w, h, static_cast<T*>(ext_[0]), static_cast<T*>(ext_[1]),
+          static_cast<T*>(ext_[2]), static_cast<T*>(ext_[3]), static_cast<T*>(ext_[4]),
+          static_cast<T*>(ext_[5]), out, num_sms_, cs_);
+    else
+      launches_ += dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h, out, num_sms_, cs_);
     IMB_CUDA(cudaGetLastError());
     std::swap(x_, xn_);
     return;
@@ -462,7 +471,7 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   IMB_CUDA(cudaEventRecord(t0, cs_));
   if (!static_halo_ok_) exchange_static();
   ev_used_ = 0;
-  const bool overlap = multi && tmp_[0] == nullptr && ni_ > 2 * R_;
+  const bool overlap = multi && opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
   for (int s = 0; s < steps; ++s) {
     if (overlap) {
       step_overlapped();
@@ -551,7 +560,7 @@ void Team::step_host(const void* x_in, void* x_out) {
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
   IMB_CUDA(cudaSetDevice(device_));
   if (!static_halo_ok_) exchange_static();
-  if (!(nccl_ && nccl_->nranks() > 1) && tmp_[0] == nullptr && ni_ >= 4 * R_) {
+  if (!(nccl_ && nccl_->nranks() > 1) && opt_.iord == 2 && tmp_[0] == nullptr && ni_ >= 4 * R_) {
     step_host_pipelined(x_in, x_out);
     return;
   }
@@ -601,7 +610,7 @@ void Team::group_pull() {
     for (int f = 1; f <= 4; ++f) pull_from_ring(f, cs_);
     static_halo_ok_ = true;
   }
-  group_overlap_ = tmp_[0] == nullptr && ni_ > 2 * R_;
+  group_overlap_ = opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
   if (!group_overlap_) {
     pull_from_ring(0, cs_);
     return;

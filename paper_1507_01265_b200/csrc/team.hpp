@@ -119,6 +119,7 @@ class Team {
   void* x0_ = nullptr;
   void* st_[4] = {nullptr, nullptr, nullptr, nullptr};  // u, v, w, h
   void* tmp_[12] = {};  // iterates, 2 velocity sets, mx, mn, bu, bd
+  void* ext_[6] = {};   // fused IORD=3: psi^(2), mx, mn, limited u, v, w
   bool static_halo_ok_ = false;
   std::int64_t launches_ = 0;
   Team* left_ = nullptr;

@@ -218,8 +218,22 @@ def test_fused_kernel_parity(orc, fp64, nonos, shape):
     assert rel_err(got, want) <= TOL[fp64]
 
 
+@pytest.mark.parametrize("fp64", [True, False])
+@pytest.mark.parametrize("shape", [(12, 5, 32), (17, 13, 64), (20, 40, 128), (11, 3, 128)])
+def test_fused_iord3_parity(orc, fp64, shape):
+    # BASELINE config 5's scheme (IORD=3 + limiter) through the two fused
+    # launches (pass 2 writing limited velocities and bounds, then pass 3).
+    opts = Options(iord=3, nonos=True, fp64=fp64)
+    dt = np.float64 if fp64 else np.float32
+    f = orc.init_fields(2, *shape, seed=29, dtype=dt)
+    got = gpu_run(f, opts, 3)
+    want = oracle_run(orc, f, opts, 3)
+    assert rel_err(got, want) <= TOL[fp64]
+
+
 @pytest.mark.parametrize("shares", [[16, 16], [9, 7, 16], [6, 26], [8, 8, 8, 8]])
-@pytest.mark.parametrize("opts", [Options(2, True, True), Options(2, False, False)])
+@pytest.mark.parametrize("opts", [Options(2, True, True), Options(2, False, False),
+                                  Options(3, True, True)])
 def test_group_decomposition_fused_is_bit_identical(shares, opts):
     n, m, l = sum(shares), 20, 64
     with Team(n, m, l, opts) as t:
