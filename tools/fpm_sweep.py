@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--gran", type=int, default=8)
     ap.add_argument("--out", default="gpurun_out/fpm")
     ap.add_argument("--validate-steps", type=int, default=100)
+    ap.add_argument("--table-max", type=int, default=48, help="largest Delta of the table")
     a = ap.parse_args()
     if a.config == "c3":  # n x 512 x 128 fp64 nonos IORD2, n in powers of two
         m, l, total = 512, 128, 1024
@@ -119,9 +120,36 @@ def main():
             report[key]["measured_speedup_vs_even"] = me / mk
             report[key]["predicted_speedup_vs_even"] = (
                 pe.makespan / report[key]["predicted_makespan_s"])
+    # Validation table in the paper's Table 1-3 format (PAPER.md:368-472,
+    # SPEC.md:369-377): symmetric offsets Delta around n/p (even processors at
+    # n/p - Delta, odd at n/p + Delta), theoretical (model) vs experimental
+    # (measured) step makespan, per-share times, speedup vs Delta = 0, and the
+    # model's prediction error.
+    table = []
+    cache = dict(per_e)
+    for d in range(0, a.table_max + 1, a.gran):
+        lo_, hi_ = base - d, base + d
+        if lo_ < min(xs) or hi_ > max(xs):
+            break
+        for s_ in (lo_, hi_):
+            if s_ not in cache:
+                cache[s_] = measure(s_, m, l, opts, a.validate_steps, a.ci, 3, 8)[0].mean
+        theo = max(fpm.eval_time(f, lo_), fpm.eval_time(f, hi_))
+        exp_ = max(cache[lo_], cache[hi_])
+        table.append(dict(delta=d, shares=[lo_, hi_], t_theory_s=theo, t_exp_s=exp_,
+                          t_even_share_s=cache[lo_], t_odd_share_s=cache[hi_],
+                          speedup_theory=pe.makespan / theo, speedup_exp=me / exp_,
+                          prediction_error=(theo - exp_) / exp_))
+    report["validation_table"] = table
     out.with_suffix(".json").write_text(json.dumps(report, indent=1) + "\n")
     print(json.dumps({k: report[k] for k in ("even", "paired", "general", "condition_satisfied",
                                              "shape")}, indent=1))
+    print(f"{'Delta':>6} {'shares':>12} {'t_theory[ms]':>13} {'t_exp[ms]':>10} "
+          f"{'speedup':>8} {'err':>7}")
+    for row in table:
+        print(f"{row['delta']:6d} {str(row['shares']):>12} {row['t_theory_s']*1e3:13.4f} "
+              f"{row['t_exp_s']*1e3:10.4f} {row['speedup_exp']:8.4f} "
+              f"{100*row['prediction_error']:6.2f}%")
 
 
 if __name__ == "__main__":
