@@ -309,6 +309,7 @@ int imb_group_run(imb_group* g, int steps, double* per_team_s, double* wall_s) {
       for (auto& t : g->teams) t->group_mark_ready();
       for (auto& t : g->teams) t->group_pull();
       for (auto& t : g->teams) t->group_compute();
+      for (auto& t : g->teams) t->group_finish();
     }
     double wall = 0.0;
     for (std::size_t q = 0; q < nt; ++q) {

@@ -81,6 +81,15 @@ struct Args {
   T* uo;
   T* vo;
   T* wo;
+  // Halo push (epilogue of the final pass): output planes t < R are also
+  // stored into the left neighbour's next-step buffer at its right-halo plane
+  // lo_ni + t, planes t >= ni - R into the right neighbour's left halo at
+  // t - ni. The neighbour may be this slab itself (periodic single slab) or
+  // another slab's buffer (same GPU, or a peer GPU over NVLink).
+  T* push_lo;
+  T* push_hi;
+  int lo_ni;
+  int ni;
 };
 
 // ---- per-lane vectors of K consecutive k values ---------------------------
@@ -736,6 +745,34 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       nb_sync();
     }
   }
+  // Halo push epilogue (outside the streaming loop so the hot loop's
+  // schedule is untouched): re-read this block's output planes t < R and
+  // t >= ni - R of its own tile rows (written above by this block; visible
+  // after the barrier) and store them into the neighbours' halo planes.
+  if constexpr (MODE != 1) {
+    if (a.push_lo != nullptr || a.push_hi != nullptr) {
+      __syncthreads();
+      const int tl = (ib > 0 ? ib : 0), th = (ie < a.R ? ie : a.R);          // [tl, th): t < R
+      const int ul = (ib > a.ni - a.R ? ib : a.ni - a.R), uh = ie;           // t >= ni - R
+      for (int pass = 0; pass < 2; ++pass) {
+        const int p0 = pass == 0 ? tl : ul, p1 = pass == 0 ? th : uh;
+        T* dstb = pass == 0 ? a.push_lo : a.push_hi;
+        if (dstb == nullptr) continue;
+        for (int t = p0; t < p1; ++t) {
+          const long long dplane = pass == 0 ? static_cast<long long>(a.R + a.lo_ni + t)
+                                             : static_cast<long long>(a.R + t - a.ni);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const int rr = c / NS, k0 = k0of(c);
+            const int r = warp * RW + rr;
+            if (r < C::HALO || r >= RR - C::HALO || j0 + r - C::HALO >= m) continue;
+            const int g = gj[rr] + k0;
+            vstore(dstb + dplane * a.plane + g, vload<T, K>(a.out + pl(t) + g));
+          }
+        }
+      }
+    }
+  }
 #undef KMG
 #undef KPG
 #undef KMS
@@ -823,9 +860,11 @@ extern "C" int imb_debug_phase_cycles(unsigned long long* out, int reset) {
 
 template <class T>
 int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
-                 const T* w, const T* h, T* out, int num_sms, cudaStream_t st) {
+                 const T* w, const T* h, T* out, int num_sms, cudaStream_t st,
+                 const HaloPush<T>& push) {
   if (iord != 2) return 0;
-  Args<T> a{x, u, v, w, h, out, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+  Args<T> a{x, u, v, w, h, out, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
+            push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
   return nonos ? dispatch_l<T, true, 0>(fs, a, num_sms, st)
                : dispatch_l<T, false, 0>(fs, a, num_sms, st);
 }
@@ -833,30 +872,34 @@ int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T*
 template <class T>
 int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w,
                   const T* h, T* x2, T* mx, T* mn, T* u2, T* v2, T* w2, T* out, int num_sms,
-                  cudaStream_t st) {
+                  cudaStream_t st, const HaloPush<T>& push) {
   // pass 2 (with the donor) over the output planes widened by the radius of
   // the limited pass 3 (2), then pass 3 on the requested planes.
   FusedShape f1 = fs;
   f1.o0 = fs.o0 - 2;
   f1.o1 = fs.o1 + 2;
-  Args<T> a1{x, u, v, w, h, x2, 0, 0, 0, 0, 0, 0, 0, mx, mn, u2, v2, w2};
+  Args<T> a1{x, u, v, w, h, x2, 0, 0, 0, 0, 0, 0, 0, mx, mn, u2, v2, w2,
+             nullptr, nullptr, 0, static_cast<int>(fs.ni)};
   int n = dispatch_l<T, true, 1>(f1, a1, num_sms, st);
-  Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr};
+  Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr,
+             push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
   n += dispatch_l<T, true, 2>(fs, a2, num_sms, st);
   return n;
 }
 
 template int launch_fused<double>(const FusedShape&, int, int, const double*, const double*,
                                   const double*, const double*, const double*, double*, int,
-                                  cudaStream_t);
+                                  cudaStream_t, const HaloPush<double>&);
 template int launch_fused<float>(const FusedShape&, int, int, const float*, const float*,
                                  const float*, const float*, const float*, float*, int,
-                                 cudaStream_t);
+                                 cudaStream_t, const HaloPush<float>&);
 template int launch_fused3<double>(const FusedShape&, const double*, const double*, const double*,
                                    const double*, const double*, double*, double*, double*,
-                                   double*, double*, double*, double*, int, cudaStream_t);
+                                   double*, double*, double*, double*, int, cudaStream_t,
+                                   const HaloPush<double>&);
 template int launch_fused3<float>(const FusedShape&, const float*, const float*, const float*,
                                   const float*, const float*, float*, float*, float*, float*,
-                                  float*, float*, float*, int, cudaStream_t);
+                                  float*, float*, float*, int, cudaStream_t,
+                                  const HaloPush<float>&);
 
 }  // namespace imb::dev

@@ -48,16 +48,25 @@ struct FusedShape {
   std::int64_t ni, R;     // interior planes, halo planes of the padded slab
   std::int64_t o0, o1;    // output plane range, local interior coordinates
 };
+// Halo push targets of a fused step (see mpdata_fused.cu Args): the
+// neighbours' next-step buffers (padded-slab base pointers); null = none.
+template <class T>
+struct HaloPush {
+  T* lo = nullptr;          // left neighbour's output buffer
+  std::int64_t lo_ni = 0;   // left neighbour's interior planes
+  T* hi = nullptr;          // right neighbour's output buffer
+};
 // True when the fused kernel supports this (iord, nonos, m, l) combination.
 bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool fp64);
 template <class T>
 int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
-                 const T* w, const T* h, T* out, int num_sms, cudaStream_t st);
+                 const T* w, const T* h, T* out, int num_sms, cudaStream_t st,
+                 const HaloPush<T>& push = {});
 // IORD=3 + limiter as two fused launches: donor + pass 2 (writing psi^(2),
 // its limited velocities and bounds on planes widened by 2), then pass 3.
 template <class T>
 int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, const T* w,
                   const T* h, T* x2, T* mx, T* mn, T* u2, T* v2, T* w2, T* out, int num_sms,
-                  cudaStream_t st);
+                  cudaStream_t st, const HaloPush<T>& push = {});
 
 }  // namespace imb::dev

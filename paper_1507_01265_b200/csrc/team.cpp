@@ -219,9 +219,11 @@ void Team::init_recipe(int kind, std::uint64_t seed) {
                            cudaMemcpyDeviceToDevice, cs_));
   IMB_CUDA(cudaStreamSynchronize(cs_));
   static_halo_ok_ = true;  // recipe halos are generated, not exchanged
+  halo_fresh_ = true;
 }
 
 void Team::upload(int field, const void* host, std::size_t bytes) {
+  halo_fresh_ = false;
   const std::size_t want = static_cast<std::size_t>(ni_) * plane_bytes();
   if (bytes != want)
     throw ContractError("upload of " + std::to_string(bytes) + " bytes, slab needs " +
@@ -249,6 +251,7 @@ void Team::download(int field, void* host, std::size_t bytes) {
 }
 
 void Team::reset() {
+  halo_fresh_ = false;
   IMB_CUDA(cudaSetDevice(device_));
   IMB_CUDA(cudaMemcpyAsync(x_, x0_, static_cast<std::size_t>(P_) * plane_bytes(),
                            cudaMemcpyDeviceToDevice, cs_));
@@ -340,15 +343,18 @@ void Team::compute_step_t() {
   T* out = static_cast<T*>(xn_);
   if (tmp_[0] == nullptr) {
     dev::FusedShape fs{m_, l_, ni_, R_, 0, ni_};
+    dev::HaloPush<T> push{static_cast<T*>(push_lo_), push_lo_ni_, static_cast<T*>(push_hi_)};
     if (opt_.iord == 3)
       launches_ += dev::launch_fused3<T>(
           fs, x, u, v, w, h, static_cast<T*>(ext_[0]), static_cast<T*>(ext_[1]),
           static_cast<T*>(ext_[2]), static_cast<T*>(ext_[3]), static_cast<T*>(ext_[4]),
-          static_cast<T*>(ext_[5]), out, num_sms_, cs_);
+          static_cast<T*>(ext_[5]), out, num_sms_, cs_, push);
     else
-      launches_ += dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h, out, num_sms_, cs_);
+      launches_ += dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h, out, num_sms_,
+                                        cs_, push);
     IMB_CUDA(cudaGetLastError());
-    std::swap(x_, xn_);
+    push_lo_ = push_hi_ = nullptr;
+    if (swap_after_) std::swap(x_, xn_);
     return;
   }
   T* it[2] = {static_cast<T*>(tmp_[0]), static_cast<T*>(tmp_[1])};
@@ -447,6 +453,7 @@ void Team::fused_range(std::int64_t o0, std::int64_t o1) {
 // exchange event. The next step's sends read planes written by the boundary
 // launches, which the ev_ready record at the top of that step orders.
 void Team::step_overlapped() {
+  halo_fresh_ = false;
   IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
   IMB_CUDA(cudaStreamWaitEvent(xs_, ev_ready_, 0));
   nccl_->swap_halos(static_cast<char*>(x_), plane_bytes(), R_, ni_, xs_);
@@ -472,9 +479,23 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   if (!static_halo_ok_) exchange_static();
   ev_used_ = 0;
   const bool overlap = multi && opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
+  const bool self_push = !multi && tmp_[0] == nullptr;
   for (int s = 0; s < steps; ++s) {
     if (overlap) {
       step_overlapped();
+      continue;
+    }
+    if (self_push) {
+      // Periodic single slab: the kernel's epilogue writes the edge planes
+      // into the opposite halos of its own output, so after the first step
+      // no exchange is needed at all.
+      if (!halo_fresh_) exchange_x_self(x_);
+      push_lo_ = push_hi_ = xn_;
+      push_lo_ni_ = ni_;
+      begin_compute_window();
+      compute_step();
+      end_compute_window();
+      halo_fresh_ = true;
       continue;
     }
     if (multi)
@@ -485,6 +506,7 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
     compute_step();
     end_compute_window();
   }
+  if (!self_push) halo_fresh_ = false;
   IMB_CUDA(cudaEventRecord(t1, cs_));
   IMB_CUDA(cudaEventSynchronize(t1));
   float ms = 0.f;
@@ -557,6 +579,7 @@ void Team::step_host_pipelined(const void* x_in, void* x_out) {
 }
 
 void Team::step_host(const void* x_in, void* x_out) {
+  halo_fresh_ = false;
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
   IMB_CUDA(cudaSetDevice(device_));
   if (!static_halo_ok_) exchange_static();
@@ -604,40 +627,42 @@ void Team::group_mark_ready() {
 
 void Team::group_pull() {
   IMB_CUDA(cudaSetDevice(device_));
+  // Both neighbours finished the previous step: their edge planes are final
+  // and their kernels no longer read the buffers this step writes into.
   IMB_CUDA(cudaStreamWaitEvent(cs_, left_->ev_ready_, 0));
   IMB_CUDA(cudaStreamWaitEvent(cs_, right_->ev_ready_, 0));
   if (!static_halo_ok_) {
     for (int f = 1; f <= 4; ++f) pull_from_ring(f, cs_);
     static_halo_ok_ = true;
   }
-  group_overlap_ = opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
-  if (!group_overlap_) {
-    pull_from_ring(0, cs_);
-    return;
-  }
-  // Same split as the NCCL path: the pull runs on the exchange stream after
-  // both neighbours and this team finished the previous step.
-  IMB_CUDA(cudaStreamWaitEvent(xs_, left_->ev_ready_, 0));
-  IMB_CUDA(cudaStreamWaitEvent(xs_, right_->ev_ready_, 0));
-  IMB_CUDA(cudaStreamWaitEvent(xs_, ev_ready_, 0));
-  IMB_CUDA(cudaStreamWaitEvent(xs_, ev_static_, 0));
-  pull_from_ring(0, xs_);
-  IMB_CUDA(cudaEventRecord(ev_halo_, xs_));
+  // Fused slabs push their edge planes into the neighbours' halos from the
+  // kernel epilogue; a copy is only needed when x's halos are stale.
+  if (tmp_[0] != nullptr || !halo_fresh_) pull_from_ring(0, cs_);
 }
 
 void Team::group_compute() {
   IMB_CUDA(cudaSetDevice(device_));
   begin_compute_window();
-  if (group_overlap_) {
-    fused_range(R_, ni_ - R_);
-    IMB_CUDA(cudaStreamWaitEvent(cs_, ev_halo_, 0));
-    fused_range(0, R_);
-    fused_range(ni_ - R_, ni_);
-    std::swap(x_, xn_);
+  if (tmp_[0] == nullptr) {
+    // push targets: the neighbours' output buffers of this step (their
+    // pointers are swapped only in group_finish, after every launch)
+    push_lo_ = left_->xn_;
+    push_lo_ni_ = left_->ni_;
+    push_hi_ = right_->xn_;
+    swap_after_ = false;
+    compute_step();
+    swap_after_ = true;
   } else {
     compute_step();
   }
   end_compute_window();
+}
+
+void Team::group_finish() {
+  if (tmp_[0] == nullptr) {
+    std::swap(x_, xn_);
+    halo_fresh_ = true;
+  }
 }
 
 }  // namespace imb::rt

@@ -73,6 +73,7 @@ class Team {
   void group_mark_ready();
   void group_pull();
   void group_compute();
+  void group_finish();  // phase 4: swap the ping-pong buffers (fused push path)
 
   std::int64_t launches() const { return launches_; }
   int device() const { return device_; }
@@ -121,6 +122,14 @@ class Team {
   void* tmp_[12] = {};  // iterates, 2 velocity sets, mx, mn, bu, bd
   void* ext_[6] = {};   // fused IORD=3: psi^(2), mx, mn, limited u, v, w
   bool static_halo_ok_ = false;
+  // Halo push of the next fused launch (consumed by it) and whether x's halo
+  // planes already hold the neighbours' edge planes (written by the previous
+  // step's push), so no exchange is needed before the next step.
+  void* push_lo_ = nullptr;
+  void* push_hi_ = nullptr;
+  std::int64_t push_lo_ni_ = 0;
+  bool halo_fresh_ = false;
+  bool swap_after_ = true;
   std::int64_t launches_ = 0;
   Team* left_ = nullptr;
   Team* right_ = nullptr;
