@@ -77,3 +77,24 @@ def test_step_radius():
     assert _lib.load().imb_step_radius(C.byref(bad)) == -_lib.ConfigError.code
     h = C.c_void_p()
     assert _lib.load().imb_team_create(None, None, 0, 0, 0, C.byref(h)) == _lib.ContractError.code
+
+
+def _demo():
+    subprocess.run(["make", "-s", "-C", str(ROOT / "paper_1507_01265_b200" / "csrc"), "demo"],
+                   check=True)
+    return ROOT / "tests" / "cpp" / "api_demo"
+
+
+def test_cpp_caller_links_reference_named_api():
+    # A C++ program written against include/imbalance/*.hpp (the reference's
+    # names) builds and links against libimb_b200.so; its FPM part runs here.
+    out = subprocess.run([str(_demo()), "cpu"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "cpu part: ok" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_caller_runs_workload_on_gpu():
+    out = subprocess.run([str(_demo()), "gpu"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "gpu part: ok" in out.stdout
