@@ -48,11 +48,13 @@ __device__ unsigned long long g_phase_cycles[10];
 #define IMB_ACC(slot, a, b)
 #endif
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR = 1>
 struct Cfg {
-  static constexpr int KPT = L / (32 * NS);       // consecutive k per lane and segment
-  static_assert(KPT * 32 * NS == L, "row must split into NS warp-wide segments");
-  static constexpr int RR = NW * RW;              // region rows
+  // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
+  static constexpr int KPT = L / (32 * NS * WPR);  // consecutive k per lane and segment
+  static_assert(KPT * 32 * NS * WPR == L, "row must split into warp-wide segments");
+  static_assert(WPR == 1 || RW == 1, "several warps per row take one row each");
+  static constexpr int RR = NW * RW / WPR;         // region rows
   static constexpr int HALO = NONOS ? 2 : 1;      // recomputed rows on each side
   static constexpr int TJ = RR - 2 * HALO;        // output rows per tile
   static constexpr int NT = NW * 32;
@@ -203,9 +205,9 @@ __device__ __forceinline__ Vec<T, K> vabs(const Vec<T, K>& a) {
 // IORD=3 step, additionally writing the pass's limited velocities and 7-point
 // bounds. MODE 2: the second corrective pass from psi^(2) (read instead of the
 // donor), the limited velocities (as u, v, w) and the accumulated bounds.
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, int WPR>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS, WPR>;
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS;
   using V = Vec<T, K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -225,13 +227,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   const int j0 = tile * C::TJ;
   const int m = a.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wrow = (warp / WPR) * RW;        // first region row of this warp
+  const int wcol = (warp % WPR) * (L / WPR);  // first k of this warp's row part
 
   // Rows of this warp: region row r = warp*RW + rr; global row offsets (j
   // wraps periodically) of the row and its j-1 / j+1 neighbours.
   int gj[RW], gjm[RW], gjp[RW];
 #pragma unroll
   for (int rr = 0; rr < RW; ++rr) {
-    int j = j0 - C::HALO + warp * RW + rr;
+    int j = j0 - C::HALO + wrow + rr;
     j = ((j % m) + m) % m;
     gj[rr] = j * L;
     gjm[rr] = (j == 0 ? m - 1 : j - 1) * L;
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   auto slot3 = [](int p) { return (p + 6) % 3; };  // p >= -3
   auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
   // cell group c = (row rr, segment sg): first k of this lane in the segment
-  auto k0of = [&](int c) { return (c % NS) * 32 * K + lane * K; };
+  auto k0of = [&](int c) { return wcol + (c % NS) * 32 * K + lane * K; };
   // MODE 1: plane t+1 values of an own tile row are stored once (segments
   // abut: this block owns planes [ib, ie), the last segment also plane o1).
   auto keep = [&](int t, int r) {
@@ -253,10 +257,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // 3-4x slower than the hardware barrier and removed.)
   auto nb_sync = [&]() { __syncthreads(); };
   // neighbour helpers: G = global source row, S = shared source row
-#define KMG(vec, row, k0) kminus<L, NS, true>(vec, row, k0, lane)
-#define KPG(vec, row, k0) kplus<L, NS, true>(vec, row, k0, lane)
-#define KMS(vec, row, k0) kminus<L, NS, false>(vec, row, k0, lane)
-#define KPS(vec, row, k0) kplus<L, NS, false>(vec, row, k0, lane)
+#define KMG(vec, row, k0) kminus<L, NS * WPR, true>(vec, row, k0, lane)
+#define KPG(vec, row, k0) kplus<L, NS * WPR, true>(vec, row, k0, lane)
+#define KMS(vec, row, k0) kminus<L, NS * WPR, false>(vec, row, k0, lane)
+#define KPS(vec, row, k0) kplus<L, NS * WPR, false>(vec, row, k0, lane)
 
   V nmx_new[NC], nmn_new[NC], nmx[NC], nmn[NC];  // psi^n star extrema (STARC)
 
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       for (int c = 0; c < NC; ++c) {
         const int rr = c / NS, k0 = k0of(c);
         const int g = gj[rr] + k0;
-        vstore(dst + (warp * RW + rr) * L + k0, vload<T, K>(X + g));
+        vstore(dst + (wrow + rr) * L + k0, vload<T, K>(X + g));
         if constexpr (STARC) {
           nmx_new[c] = vload<T, K>(a.mxo + pl(p) + g);
           nmn_new[c] = vload<T, K>(a.mno + pl(p) + g);
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int rr = c / NS, k0 = k0of(c);
-      const int r = warp * RW + rr;
+      const int r = wrow + rr;
       const int g = gj[rr] + k0;
       const V xc = vload<T, K>(X + g);
       const V xm = vload<T, K>(Xm + g), xp = vload<T, K>(Xp + g);
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int rr = c / NS, k0 = k0of(c);
-      const int r = warp * RW + rr;
+      const int r = wrow + rr;
       if (r < 1) continue;  // warp-uniform
       const bool row_u = r < RR - 1;  // x/z faces (y faces: every r >= 1)
       const int g = gj[rr] + k0;
@@ -533,7 +537,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const int rr = c / NS, k0 = k0of(c);
-          const int r = warp * RW + rr;
+          const int r = wrow + rr;
           if (r < 1 || r >= RR - 1) continue;
           const int so = r * L + k0;
           const V xc = sload<T, K>(s1 + so);
@@ -624,7 +628,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const int rr = c / NS, k0 = k0of(c);
-          const int r = warp * RW + rr;
+          const int r = wrow + rr;
           if (r < 2 || r >= RR - 1) continue;
           const int so = r * L + k0;
           const V bu = sload<T, K>(buA + so), bd = sload<T, K>(bdA + so);
@@ -714,7 +718,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int rr = c / NS, k0 = k0of(c);
-        const int r = warp * RW + rr;
+        const int r = wrow + rr;
         if (r < 1 || r >= RR - 1) continue;
         const int so = r * L + k0;
         const V xc = sload<T, K>(s0 + so);
@@ -764,7 +768,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             const int rr = c / NS, k0 = k0of(c);
-            const int r = warp * RW + rr;
+            const int r = wrow + rr;
             if (r < C::HALO || r >= RR - C::HALO || j0 + r - C::HALO >= m) continue;
             const int g = gj[rr] + k0;
             vstore(dstb + dplane * a.plane + g, vload<T, K>(a.out + pl(t) + g));
@@ -801,10 +805,10 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   return best;
 }
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, int WPR = 1>
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS>;
-  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS, WPR>;
+  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, WPR>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
@@ -833,7 +837,12 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
   // psi^n star; fp32 holds 4 floats per lane and carries the star.
   constexpr bool D = sizeof(T) == 8;
   switch (fs.l) {
-    case 128: return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+    case 128:
+#ifdef IMB_FUSED_VARIANTS
+      if (std::getenv("IMB_WPR2"))  // 32 warps, 2 per row, 2 x 32 cells each
+        return launch_cfg<T, 128, 1, 32, 2, NONOS, false, MODE, 2>(fs, a, num_sms, st);
+#endif
+      return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     default: return 0;
