@@ -193,6 +193,25 @@ __device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, const T* row, int
   for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
   return r;
 }
+// k-1 / k+1 of a vector held in shared memory: the single out-of-vector
+// element is read back from the row (periodic wrap in the address), so no
+// shuffle and no edge-lane special case.
+template <int L, class T, int K>
+__device__ __forceinline__ Vec<T, K> kminus_s(const Vec<T, K>& a, const T* row, int k0) {
+  Vec<T, K> r;
+  r.e[0] = row[k0 == 0 ? L - 1 : k0 - 1];
+#pragma unroll
+  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
+  return r;
+}
+template <int L, class T, int K>
+__device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* row, int k0) {
+  Vec<T, K> r;
+  r.e[K - 1] = row[k0 + K == L ? 0 : k0 + K];
+#pragma unroll
+  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
+  return r;
+}
 template <class T, int K>
 __device__ __forceinline__ Vec<T, K> vabs(const Vec<T, K>& a) {
   Vec<T, K> r;
@@ -259,8 +278,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // neighbour helpers: G = global source row, S = shared source row
 #define KMG(vec, row, k0) kminus<L, NS * WPR, true>(vec, row, k0, lane)
 #define KPG(vec, row, k0) kplus<L, NS * WPR, true>(vec, row, k0, lane)
+#ifndef IMB_SMEM_RELOAD  // shuffles measured faster than k+-1 smem reloads (C2 -7%)
 #define KMS(vec, row, k0) kminus<L, NS * WPR, false>(vec, row, k0, lane)
 #define KPS(vec, row, k0) kplus<L, NS * WPR, false>(vec, row, k0, lane)
+#else
+#define KMS(vec, row, k0) kminus_s<L>(vec, row, k0)
+#define KPS(vec, row, k0) kplus_s<L>(vec, row, k0)
+#endif
 
   V nmx_new[NC], nmn_new[NC], nmx[NC], nmn[NC];  // psi^n star extrema (STARC)
 
@@ -841,6 +865,12 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
 #ifdef IMB_FUSED_VARIANTS
       if (std::getenv("IMB_WPR2"))  // 32 warps, 2 per row, 2 x 32 cells each
         return launch_cfg<T, 128, 1, 32, 2, NONOS, false, MODE, 2>(fs, a, num_sms, st);
+      if (const char* e = std::getenv("IMB_NW")) {  // fewer region rows, more registers
+        const int nw = std::atoi(e);
+        if (nw == 14) return launch_cfg<T, 128, 1, 14, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (nw == 12) return launch_cfg<T, 128, 1, 12, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (nw == 20) return launch_cfg<T, 128, 1, 20, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+      }
 #endif
       return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
