@@ -149,7 +149,6 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
   IMB_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
   IMB_CUDA(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming));
   IMB_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
-  IMB_CUDA(cudaEventCreateWithFlags(&ev_static_, cudaEventDisableTiming));
   const std::size_t fbytes = static_cast<std::size_t>(P_) * plane_bytes();
   // The fused kernels take any slab >= R planes (they read R halo planes);
   // every slab of a decomposition then runs the same arithmetic.
@@ -181,14 +180,12 @@ Team::~Team() {
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   if (ev_ready_) cudaEventDestroy(ev_ready_);
   if (ev_halo_) cudaEventDestroy(ev_halo_);
-  if (ev_static_) cudaEventDestroy(ev_static_);
   if (cs_) cudaStreamDestroy(cs_);
   if (xs_) cudaStreamDestroy(xs_);
   if (ups_) cudaStreamDestroy(ups_);
   if (dns_) cudaStreamDestroy(dns_);
   for (cudaEvent_t e : ev_pipe_) cudaEventDestroy(e);
   if (pool_) cudaFree(pool_);
-  if (host_stage_) cudaFreeHost(host_stage_);
 }
 
 void* Team::fbuf(int field) const {
@@ -622,7 +619,6 @@ void Team::connect_nccl(const unsigned char* id, int nranks, int rank) {
 void Team::group_mark_ready() {
   IMB_CUDA(cudaSetDevice(device_));
   IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
-  IMB_CUDA(cudaEventRecord(ev_static_, cs_));
 }
 
 void Team::group_pull() {

@@ -65,11 +65,14 @@ class Team {
     right_ = right;
   }
 
-  // Group stepping, issued by imb_group in three host phases per step, each
-  // phase over all teams before the next: (1) record "x of this step is
-  // complete", (2) wait for both neighbours and pull their edge planes into
-  // the halos, (3) compute and swap. Phase 2 reads the neighbours' current
-  // x buffers, so it must precede every phase-3 swap of the step.
+  // Group stepping, issued by imb_group in four host phases per step, each
+  // over all teams before the next: (1) record "x of this step is complete";
+  // (2) wait for both neighbours, then (staged slabs, or stale halos) pull
+  // their edge planes into the halos; (3) launch the step — fused slabs push
+  // their edge planes into the neighbours' next-step halos from the kernel
+  // epilogue, targeting the neighbours' current output buffers; (4) swap.
+  // The swap is deferred to phase 4 so phase 3 sees every team's buffers of
+  // this step.
   void group_mark_ready();
   void group_pull();
   void group_compute();
@@ -109,8 +112,7 @@ class Team {
   std::int64_t i0_, ni_, R_, P_;
   int num_sms_ = 148;
   cudaStream_t cs_ = nullptr, xs_ = nullptr;  // compute, exchange
-  cudaEvent_t ev_ready_ = nullptr, ev_halo_ = nullptr, ev_static_ = nullptr;
-  bool group_overlap_ = false;
+  cudaEvent_t ev_ready_ = nullptr, ev_halo_ = nullptr;
   std::vector<cudaEvent_t> ev_pool_;  // begin/end pairs of compute windows
   std::size_t ev_used_ = 0;
   // device buffers (padded slabs of P_ planes)
@@ -134,7 +136,6 @@ class Team {
   Team* left_ = nullptr;
   Team* right_ = nullptr;
   std::unique_ptr<NcclLink> nccl_;
-  void* host_stage_ = nullptr;  // pinned staging for step_host
 };
 
 }  // namespace imb::rt
