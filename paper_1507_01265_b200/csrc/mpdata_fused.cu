@@ -312,8 +312,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       }
       return;
     }
+    const int nc_donor = MODE == 2 ? 0 : NC;  // (MODE 2 returned above)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
+    for (int c = 0; c < nc_donor; ++c) {
       const int rr = c / NS, k0 = k0of(c);
       const int r = wrow + rr;
       const int g = gj[rr] + k0;
