@@ -172,6 +172,14 @@ int imb_average(int64_t unit_cells, int64_t granularity, const imb_speed_sample*
 int imb_scaled(int64_t unit_cells, int64_t granularity, const imb_speed_sample* s, int ns,
                double factor, imb_speed_sample* out);
 
+/* slice_surface, fpm.hpp:123 (+ SpeedSurface::validate, fpm.hpp:81-91): the
+ * surface is nn x nm samples, row-major in n (samples[i*nm + j].x must equal
+ * m_values[j]); out receives the nm samples of row fixed_n and
+ * *out_unit_cells = fixed_n * unit_cells. */
+int imb_slice_surface(int64_t unit_cells, int64_t granularity, const int64_t* n_values, int nn,
+                      const int64_t* m_values, int nm, const imb_speed_sample* samples,
+                      int64_t fixed_n, imb_speed_sample* out, int64_t* out_unit_cells);
+
 /* ---- partitioner: partition.hpp:17-72 ----------------------------------
  * shares/per_time hold `p` values; *offset = -1 when absent. */
 int imb_predict_makespan(int64_t unit_cells, int64_t granularity, const imb_speed_sample* s,

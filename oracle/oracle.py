@@ -135,6 +135,8 @@ def ref():
         lib.ref_improvement_search.argtypes = [i64, i64, SS, C.c_int, i64, P(C.c_int), P(i64),
                                                P(f64), P(i64)]
         lib.ref_average.argtypes = [i64, i64, SS, C.c_int, C.c_int, SS]
+        lib.ref_slice_surface.argtypes = [i64, i64, P(i64), C.c_int, P(i64), C.c_int, SS, i64,
+                                          SS, P(i64)]
         _ref = lib
     return _ref
 
@@ -210,3 +212,15 @@ def ref_average(unit, g, funcs):
     out = (RefSample * max(ns, 1))()
     st = ref().ref_average(unit, g, flat, nf, ns, out)
     return st, (None if st else [(o.x, o.speed, o.ci_halfwidth, o.repetitions) for o in out[:ns]])
+
+
+def ref_slice_surface(unit, g, n_values, m_values, samples, fixed_n):
+    nn, nm = len(n_values), len(m_values)
+    out = (RefSample * max(nm, 1))()
+    uc = C.c_int64()
+    st = ref().ref_slice_surface(unit, g, (C.c_int64 * max(nn, 1))(*n_values), nn,
+                                 (C.c_int64 * max(nm, 1))(*m_values), nm, _samples(samples),
+                                 fixed_n, out, C.byref(uc))
+    if st:
+        return st, None
+    return 0, (uc.value, [(o.x, o.speed, o.ci_halfwidth, o.repetitions) for o in out[:nm]])

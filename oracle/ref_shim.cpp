@@ -153,4 +153,25 @@ int ref_average(std::int64_t unit, std::int64_t g, const RefSample* s, int nf, i
   });
 }
 
+int ref_slice_surface(std::int64_t unit, std::int64_t g, const std::int64_t* nv, int nn,
+                      const std::int64_t* mv, int nm, const RefSample* s, std::int64_t fixed_n,
+                      RefSample* out, std::int64_t* out_unit) {
+  return guard([&] {
+    imb::SpeedSurface srf;
+    srf.unit_cells = unit;
+    srf.granularity = g;
+    srf.label = "ref";
+    srf.n_values.assign(nv, nv + nn);
+    srf.m_values.assign(mv, mv + nm);
+    for (int q = 0; q < nn * nm; ++q)
+      srf.samples.push_back({s[q].x, s[q].speed, s[q].ci_halfwidth, s[q].repetitions});
+    imb::SpeedFunction f = imb::slice_surface(srf, fixed_n);
+    for (std::size_t q = 0; q < f.samples().size(); ++q) {
+      const imb::SpeedSample& v = f.samples()[q];
+      out[q] = {v.x, v.speed, v.ci_halfwidth, v.repetitions};
+    }
+    *out_unit = f.unit_cells();
+  });
+}
+
 }  // extern "C"

@@ -447,6 +447,34 @@ int imb_scaled(int64_t unit, int64_t g, const imb_speed_sample* s, int ns, doubl
   });
 }
 
+int imb_slice_surface(int64_t unit, int64_t g, const int64_t* n_values, int nn,
+                      const int64_t* m_values, int nm, const imb_speed_sample* samples,
+                      int64_t fixed_n, imb_speed_sample* out, int64_t* out_unit_cells) {
+  return guard([&] {
+    need(out, "out");
+    need(out_unit_cells, "out_unit_cells");
+    if (nn < 0 || nm < 0) throw imb::ContractError("surface extents must be >= 0");
+    if (nn > 0) need(n_values, "n_values");
+    if (nm > 0) need(m_values, "m_values");
+    if (nn * nm > 0) need(samples, "samples");
+    imb::SpeedSurface srf;
+    srf.unit_cells = unit;
+    srf.granularity = g;
+    srf.label = "c-abi";
+    srf.n_values.assign(n_values, n_values + nn);
+    srf.m_values.assign(m_values, m_values + nm);
+    for (int q = 0; q < nn * nm; ++q)
+      srf.samples.push_back({samples[q].x, samples[q].speed, samples[q].ci_halfwidth,
+                             samples[q].repetitions});
+    const imb::SpeedFunction f = imb::slice_surface(srf, fixed_n);
+    for (std::size_t q = 0; q < f.samples().size(); ++q) {
+      const imb::SpeedSample& v = f.samples()[q];
+      out[q] = imb_speed_sample{v.x, v.speed, v.ci_halfwidth, v.repetitions};
+    }
+    *out_unit_cells = f.unit_cells();
+  });
+}
+
 // ---- partitioner -------------------------------------------------------------
 int imb_predict_makespan(int64_t unit, int64_t g, const imb_speed_sample* s, int ns,
                          const int64_t* shares, int p, double* per_time, double* makespan) {

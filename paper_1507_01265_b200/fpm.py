@@ -120,6 +120,30 @@ def scaled(f: SpeedFunction, factor: float) -> SpeedFunction:  # fpm.hpp:118
                                for o in out[:ns]), f.label)
 
 
+@dataclass(frozen=True)
+class SpeedSurface:  # fpm.hpp:81-91 — rectangular (n, m) grid, row-major in n
+    unit_cells: int
+    granularity: int
+    n_values: tuple
+    m_values: tuple
+    samples: tuple  # len(n_values) * len(m_values) SpeedSample, x == m_values[j]
+    label: str = ""
+
+
+def slice_surface(g: SpeedSurface, fixed_n: int) -> SpeedFunction:  # fpm.hpp:123
+    nn, nm = len(g.n_values), len(g.m_values)
+    smp = tuple(s if isinstance(s, SpeedSample) else SpeedSample(*s) for s in g.samples)
+    out = (_lib.imb_speed_sample * max(nm, 1))()
+    uc = C.c_int64()
+    check(load().imb_slice_surface(g.unit_cells, g.granularity,
+                                   (C.c_int64 * max(nn, 1))(*g.n_values), nn,
+                                   (C.c_int64 * max(nm, 1))(*g.m_values), nm,
+                                   samples_array(smp), int(fixed_n), out, C.byref(uc)))
+    return SpeedFunction(uc.value, g.granularity,
+                         tuple(SpeedSample(o.x, o.speed, o.ci_halfwidth, o.repetitions)
+                               for o in out[:nm]), f"{g.label}@n={fixed_n}")
+
+
 # ---- partitioner (partition.hpp:17-72) -------------------------------------
 @dataclass
 class PartitionProblem:

@@ -152,3 +152,27 @@ def test_t_quantile_and_summary():
     assert abs(s.ci_halfwidth - fpm.t_quantile_975(3) * sd / 2.0) <= 1e-12 * s.ci_halfwidth
     with pytest.raises(_lib.InsufficientDataError):
         fpm.summarize([1.0])
+
+
+@needs_ref
+def test_slice_surface_parity():
+    # fpm.cpp:192-222: validation errors and slicing, product vs reference.
+    rng = random.Random(12)
+    for _ in range(100):
+        nv = sorted(rng.sample(range(100, 140, 4), rng.randint(1, 4)))
+        mv = list(range(8, 8 + 4 * rng.randint(1, 6), 4))
+        smp = [(mv[j], rng.uniform(1e5, 2e6), rng.random(), rng.randint(1, 5))
+               for _ in nv for j in range(len(mv))]
+        if rng.random() < 0.2:  # corrupt one x to hit the grid check
+            q = rng.randrange(len(smp))
+            smp[q] = (smp[q][0] + 1,) + smp[q][1:]
+        fixed = rng.choice(nv + [nv[0] + 1])
+        st, want = O.ref_slice_surface(15360, 4, nv, mv, smp, fixed)
+        srf = fpm.SpeedSurface(15360, 4, tuple(nv), tuple(mv), tuple(smp), "s")
+        try:
+            f = fpm.slice_surface(srf, fixed)
+            got, gst = (f.unit_cells, [(s.x, s.speed, s.ci_halfwidth, s.repetitions)
+                                       for s in f.samples]), 0
+        except _lib.ImbError as e:
+            got, gst = None, e.code
+        assert (gst, got) == (st, want)
