@@ -129,6 +129,13 @@ int imb_group_create(const imb_domain* global, const imb_opts* opts, int nteams,
 int imb_group_destroy(imb_group* g);
 int imb_group_team(imb_group* g, int index, imb_team** out);
 int imb_group_init_recipe(imb_group* g, int recipe, uint64_t seed);
+/* Step synchronisation of a group. EVENTS (default): four stream-ordered
+ * host phases per step. FLAGS (fused slabs): each team's stream waits on
+ * device flag words its neighbours write after their step
+ * (cuStreamWaitValue64 / cuStreamWriteValue64) — no host phases, no events;
+ * the halo planes travel inside the step kernel (peer stores). */
+enum { IMB_GROUP_SYNC_EVENTS = 0, IMB_GROUP_SYNC_FLAGS = 1 };
+int imb_group_set_sync(imb_group* g, int mode);
 /* per_team_s[g] = compute seconds of team g; *wall_s = max over teams of
  * the run span including exchange waits. */
 int imb_group_run(imb_group* g, int steps, double* per_team_s, double* wall_s);

@@ -94,6 +94,7 @@ SIGNATURES = {
     "imb_group_destroy": (i32, [vp]),
     "imb_group_team": (i32, [vp, i32, P(vp)]),
     "imb_group_init_recipe": (i32, [vp, i32, C.c_uint64]),
+    "imb_group_set_sync": (i32, [vp, i32]),
     "imb_group_run": (i32, [vp, i32, P(f64), P(f64)]),
     "imb_fill_halo_clamped": (i32, [P(imb_domain), P(f64)]),
     "imb_stage_max7": (i32, [P(imb_domain), P(f64), P(f64)]),

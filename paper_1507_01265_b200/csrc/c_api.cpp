@@ -32,6 +32,7 @@ struct imb_team {
 struct imb_group {
   std::vector<std::unique_ptr<imb::rt::Team>> teams;
   std::vector<imb_team> handles;
+  int sync = 0;  // IMB_GROUP_SYNC_EVENTS / IMB_GROUP_SYNC_FLAGS
 };
 
 namespace {
@@ -285,6 +286,15 @@ int imb_group_team(imb_group* g, int index, imb_team** out) {
   });
 }
 
+int imb_group_set_sync(imb_group* g, int mode) {
+  return guard([&] {
+    need(g, "group");
+    if (mode != IMB_GROUP_SYNC_EVENTS && mode != IMB_GROUP_SYNC_FLAGS)
+      throw imb::ConfigError("unknown group sync mode " + std::to_string(mode));
+    g->sync = mode;
+  });
+}
+
 int imb_group_init_recipe(imb_group* g, int recipe, uint64_t seed) {
   return guard([&] {
     need(g, "group");
@@ -305,11 +315,20 @@ int imb_group_run(imb_group* g, int steps, double* per_team_s, double* wall_s) {
       g->teams[q]->take_compute_seconds();
       cudaEventRecord(t0[q], g->teams[q]->stream());
     }
+    bool flags = g->sync == IMB_GROUP_SYNC_FLAGS;
+    for (auto& t : g->teams) flags = flags && t->fused();
     for (int s = 0; s < steps; ++s) {
+      bool ready = flags;
+      for (auto& t : g->teams) ready = ready && t->halos_ready();
+      if (ready) {
+        for (auto& t : g->teams) t->group_flag_step();
+        continue;
+      }
+      // event-synchronised step (always the first one after init/upload)
       for (auto& t : g->teams) t->group_mark_ready();
       for (auto& t : g->teams) t->group_pull();
       for (auto& t : g->teams) t->group_compute();
-      for (auto& t : g->teams) t->group_finish();
+      for (auto& t : g->teams) t->group_finish(flags);
     }
     double wall = 0.0;
     for (std::size_t q = 0; q < nt; ++q) {

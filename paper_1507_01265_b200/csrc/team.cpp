@@ -1,6 +1,7 @@
 // GPU team runtime (team.hpp). Host C++; kernels live in csrc/*.cu.
 #include "team.hpp"
 
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -120,6 +121,33 @@ class NcclLink {
   int nranks_, rank_;
 };
 
+// ---- stream memory operations (driver API, resolved through the runtime) ---
+namespace {
+struct MemOps {
+  CUresult (*wait)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+  CUresult (*write)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+};
+MemOps& memops() {
+  static MemOps ops;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      ops.wait = reinterpret_cast<decltype(ops.wait)>(fn);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      ops.write = reinterpret_cast<decltype(ops.write)>(fn);
+  });
+  if (!ops.wait || !ops.write) throw CudaError("stream memory operations unavailable");
+  return ops;
+}
+void memop_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw CudaError(std::string(what) + " failed (CUresult " + std::to_string(r) + ")");
+}
+}  // namespace
+
 void nccl_unique_id(unsigned char* out) {
   ncclUniqueId uid;
   nccl_check(nccl().get_unique_id(&uid), "ncclGetUniqueId");
@@ -162,6 +190,8 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
                       std::to_string(device_));
   }
   IMB_CUDA(cudaMemsetAsync(pool_, 0, total, cs_));
+  IMB_CUDA(cudaMalloc(&flags_, 2 * sizeof(std::uint64_t)));
+  IMB_CUDA(cudaMemsetAsync(flags_, 0, 2 * sizeof(std::uint64_t), cs_));
   char* p = static_cast<char*>(pool_);
   x_ = p;
   xn_ = p + fbytes;
@@ -186,6 +216,7 @@ Team::~Team() {
   if (dns_) cudaStreamDestroy(dns_);
   for (cudaEvent_t e : ev_pipe_) cudaEventDestroy(e);
   if (pool_) cudaFree(pool_);
+  if (flags_) cudaFree(flags_);
 }
 
 void* Team::fbuf(int field) const {
@@ -654,11 +685,62 @@ void Team::group_compute() {
   end_compute_window();
 }
 
-void Team::group_finish() {
+// Flag-synchronised group step (fused slabs only): no host phases and no
+// events. Each step waits — in the stream front-end, no spinning kernel —
+// until both neighbours have announced the end of the previous step through
+// this team's flag words, launches the fused kernel that pushes its edge
+// planes into the neighbours' step-s output buffers (device stores; NVLink
+// for a peer GPU), then announces its own step in the neighbours' flags.
+// Every wait depends only on work issued earlier, so the ring cannot
+// deadlock. Buffers: step s writes bufs[(s+1)%2] of every team (all teams
+// step together), which lets a team address a neighbour's buffer without
+// reading its host-side pointers.
+void Team::group_flag_step() {
+  IMB_CUDA(cudaSetDevice(device_));
+  MemOps& ops = memops();
+  const std::uint64_t s = step_count_;
+  memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 0), s, CU_STREAM_WAIT_VALUE_GEQ),
+              "cuStreamWaitValue64");
+  memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 1), s, CU_STREAM_WAIT_VALUE_GEQ),
+              "cuStreamWaitValue64");
+  if (!static_halo_ok_ || !halo_fresh_)
+    throw ContractError("flag-synchronised step needs fresh halos (run an event step first)");
+  begin_compute_window();
+  push_lo_ = left_->out_buffer(s);
+  push_lo_ni_ = left_->ni_;
+  push_hi_ = right_->out_buffer(s);
+  swap_after_ = false;
+  compute_step();
+  swap_after_ = true;
+  end_compute_window();
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(left_->flags_ + 1), s + 1,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(right_->flags_ + 0), s + 1,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+  std::swap(x_, xn_);
+  ++step_count_;
+  halo_fresh_ = true;
+}
+
+void* Team::out_buffer(std::uint64_t s) const {
+  // x_/xn_ alternate every step; step s writes the buffer that is xn_ when
+  // this team has completed exactly s steps.
+  return ((s - step_count_) % 2 == 0) ? xn_ : x_;
+}
+
+void Team::group_finish(bool signal) {
   if (tmp_[0] == nullptr) {
     std::swap(x_, xn_);
     halo_fresh_ = true;
   }
+  if (signal) {  // keep the flag protocol's counters in step (flag mode after an event step)
+    MemOps& ops = memops();
+    memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(left_->flags_ + 1), step_count_ + 1,
+                          CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+    memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(right_->flags_ + 0), step_count_ + 1,
+                          CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+  }
+  ++step_count_;
 }
 
 }  // namespace imb::rt

@@ -76,7 +76,14 @@ class Team {
   void group_mark_ready();
   void group_pull();
   void group_compute();
-  void group_finish();  // phase 4: swap the ping-pong buffers (fused push path)
+  // phase 4: swap the ping-pong buffers (fused push path); with `signal`,
+  // also announce the step in the neighbours' flag words
+  void group_finish(bool signal = false);
+  bool halos_ready() const { return static_halo_ok_ && halo_fresh_; }
+  // Alternative group protocol for fused slabs: one call per team per step,
+  // synchronised through device flag words (cuStreamWaitValue/WriteValue).
+  void group_flag_step();
+  bool fused() const { return tmp_[0] == nullptr; }
 
   std::int64_t launches() const { return launches_; }
   int device() const { return device_; }
@@ -132,6 +139,9 @@ class Team {
   std::int64_t push_lo_ni_ = 0;
   bool halo_fresh_ = false;
   bool swap_after_ = true;
+  std::uint64_t* flags_ = nullptr;  // [0] left neighbour's, [1] right's finished steps
+  std::uint64_t step_count_ = 0;    // steps taken through the group protocols
+  void* out_buffer(std::uint64_t s) const;
   std::int64_t launches_ = 0;
   Team* left_ = nullptr;
   Team* right_ = nullptr;

@@ -193,6 +193,10 @@ class Group:
     def init_recipe(self, recipe: int = RECIPE_ROTCUBE, seed: int = 42):
         check(load().imb_group_init_recipe(self._h, int(recipe), C.c_uint64(seed)))
 
+    def set_sync(self, mode: str):
+        """'events' (default) or 'flags' (device flag words, fused slabs)."""
+        check(load().imb_group_set_sync(self._h, {"events": 0, "flags": 1}[mode]))
+
     def run(self, steps: int):
         per = (C.c_double * len(self.teams))()
         wall = C.c_double()

@@ -106,6 +106,26 @@ def test_group_decomposition_is_bit_identical(shares, opts):
     g.close()
 
 
+@pytest.mark.parametrize("shares", [[32], [16, 16], [9, 7, 16], [8, 8, 8, 8]])
+@pytest.mark.parametrize("opts", [Options(2, True, True), Options(2, False, False),
+                                  Options(3, True, True)])
+def test_group_flag_sync_is_bit_identical(shares, opts):
+    # Flag-synchronised ring (cuStreamWaitValue64 / WriteValue64 on device
+    # flag words, halos pushed by the step kernel): same bits as one slab.
+    n, m, l = sum(shares), 20, 64
+    with Team(n, m, l, opts) as t:
+        t.init_recipe(2, 11)
+        t.run(6)
+        single = t.download("x")
+    g = Group(n, m, l, shares, opts=opts)
+    g.set_sync("flags")
+    g.init_recipe(2, 11)
+    g.run(2)
+    g.run(4)  # continues in flag mode across calls
+    np.testing.assert_array_equal(g.download("x"), single)
+    g.close()
+
+
 def test_group_with_uploaded_fields(orc):
     opts = Options(2, True, True)
     f = orc.init_fields(0, 30, 16, 24, seed=3)
