@@ -166,6 +166,9 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--shares", default="", help="comma-separated slab shares (N>1)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "ipc"],
+                    help="N>1 halo exchange: NCCL send/recv, or the step kernel pushing "
+                         "edge planes into CUDA-IPC-mapped neighbour halos")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -194,7 +197,12 @@ def main():
     opts = mpdata.Options(iord=iord, nonos=nonos, fp64=fp64)
     team = mpdata.Team(n, m, l, opts, device=local, i0=i0, ni=shares[rank])
     team.init_recipe(recipe, 42)
-    if world > 1:
+    if world > 1 and args.halo == "ipc":
+        blobs = [None] * world
+        dist.all_gather_object(blobs, team.ipc_export())
+        team.connect_ipc(blobs[(rank - 1) % world], blobs[(rank + 1) % world], world, rank)
+        dist.barrier()
+    elif world > 1:
         uid = [mpdata.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         team.connect_nccl(uid[0], world, rank)
@@ -263,7 +271,7 @@ def main():
         "dtype": "f64" if fp64 else "f32", "data": "synthetic (seeded BASELINE recipe, device-generated)",
         "config": {"workload": desc, "grid": [n, m, l], "iord": iord, "nonos": nonos,
                    "boundary": "periodic", "shares": shares,
-                   "parallelism": f"slab{world}" + (" nccl-halo" if world > 1 else ""),
+                   "parallelism": f"slab{world}" + (f" {args.halo}-halo" if world > 1 else ""),
                    "l2": f"inputs larger than L2 (5 fields x {cells * elem >> 20} MiB)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": local_cells * elem, "d2h_bytes_per_step": local_cells * elem,

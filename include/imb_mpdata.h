@@ -109,6 +109,17 @@ enum { IMB_NCCL_ID_BYTES = 128 };
 int imb_nccl_unique_id(unsigned char id[IMB_NCCL_ID_BYTES]);
 int imb_team_connect_nccl(imb_team* t, const unsigned char id[IMB_NCCL_ID_BYTES], int nranks,
                           int rank);
+/* NVLink halo push between processes (no NCCL): every rank exports its
+ * buffers as CUDA IPC handles, the blobs are exchanged by any control plane,
+ * and each rank maps its ring neighbours'. From then on imb_team_run waits
+ * on device flag words (cuStreamWaitValue64), the step kernel stores its edge
+ * planes straight into the neighbours' halos, and the rank raises the
+ * neighbours' flags (cuStreamWriteValue64). All ranks must connect at the
+ * same step count and then step in lockstep. */
+enum { IMB_IPC_BLOB_BYTES = 512 };
+int imb_team_ipc_export(imb_team* t, unsigned char blob[IMB_IPC_BLOB_BYTES]);
+int imb_team_connect_ipc(imb_team* t, const unsigned char left[IMB_IPC_BLOB_BYTES],
+                         const unsigned char right[IMB_IPC_BLOB_BYTES], int nranks, int rank);
 /* The 4 point-to-point operations a rank issues per step (in order):
  * kinds[q] 0 = send / 1 = recv, peers[q], and the plane range
  * [first_plane[q], first_plane[q] + planes[q]) of the padded slab

@@ -88,6 +88,8 @@ SIGNATURES = {
     "imb_team_launch_count": (i64, [vp]),
     "imb_nccl_unique_id": (i32, [C.c_char_p]),
     "imb_team_connect_nccl": (i32, [vp, C.c_char_p, i32, i32]),
+    "imb_team_ipc_export": (i32, [vp, C.c_char_p]),
+    "imb_team_connect_ipc": (i32, [vp, C.c_char_p, C.c_char_p, i32, i32]),
     "imb_ring_plan": (i32, [i32, i32, i64, i64, P(i32), P(i32), P(i64), P(i64)]),
     "imb_slab_offsets": (i32, [P(i64), i32, P(i64)]),
     "imb_group_create": (i32, [P(imb_domain), P(imb_opts), i32, P(i32), P(i64), P(vp)]),

@@ -195,6 +195,22 @@ int imb_team_connect_nccl(imb_team* t, const unsigned char id[IMB_NCCL_ID_BYTES]
   });
 }
 
+int imb_team_ipc_export(imb_team* t, unsigned char blob[IMB_IPC_BLOB_BYTES]) {
+  return guard([&] {
+    need(blob, "blob");
+    team_of(t).ipc_export(blob);
+  });
+}
+
+int imb_team_connect_ipc(imb_team* t, const unsigned char left[IMB_IPC_BLOB_BYTES],
+                         const unsigned char right[IMB_IPC_BLOB_BYTES], int nranks, int rank) {
+  return guard([&] {
+    need(left, "left");
+    need(right, "right");
+    team_of(t).connect_ipc(left, right, nranks, rank);
+  });
+}
+
 int imb_ring_plan(int rank, int nranks, int64_t ni, int64_t R, int* kinds, int* peers,
                   int64_t* first_plane, int64_t* planes) {
   return guard([&] {

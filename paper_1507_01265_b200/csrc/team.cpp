@@ -190,8 +190,8 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
                       std::to_string(device_));
   }
   IMB_CUDA(cudaMemsetAsync(pool_, 0, total, cs_));
-  IMB_CUDA(cudaMalloc(&flags_, 2 * sizeof(std::uint64_t)));
-  IMB_CUDA(cudaMemsetAsync(flags_, 0, 2 * sizeof(std::uint64_t), cs_));
+  IMB_CUDA(cudaMalloc(&flags_, 4 * sizeof(std::uint64_t)));
+  IMB_CUDA(cudaMemsetAsync(flags_, 0, 4 * sizeof(std::uint64_t), cs_));
   char* p = static_cast<char*>(pool_);
   x_ = p;
   xn_ = p + fbytes;
@@ -217,6 +217,11 @@ Team::~Team() {
   for (cudaEvent_t e : ev_pipe_) cudaEventDestroy(e);
   if (pool_) cudaFree(pool_);
   if (flags_) cudaFree(flags_);
+  for (IpcPeer* p : {&ipc_left_, &ipc_right_})
+    if (p->opened) {
+      cudaIpcCloseMemHandle(p->pool);
+      cudaIpcCloseMemHandle(p->flags);
+    }
 }
 
 void* Team::fbuf(int field) const {
@@ -507,8 +512,12 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   if (!static_halo_ok_) exchange_static();
   ev_used_ = 0;
   const bool overlap = multi && opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
-  const bool self_push = !multi && tmp_[0] == nullptr;
+  const bool self_push = !multi && !ipc_ && tmp_[0] == nullptr;
   for (int s = 0; s < steps; ++s) {
+    if (ipc_) {
+      ipc_step();
+      continue;
+    }
     if (overlap) {
       step_overlapped();
       continue;
@@ -534,7 +543,7 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
     compute_step();
     end_compute_window();
   }
-  if (!self_push) halo_fresh_ = false;
+  if (!self_push && !ipc_) halo_fresh_ = false;
   IMB_CUDA(cudaEventRecord(t1, cs_));
   IMB_CUDA(cudaEventSynchronize(t1));
   float ms = 0.f;
@@ -610,6 +619,15 @@ void Team::step_host(const void* x_in, void* x_out) {
   halo_fresh_ = false;
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
   IMB_CUDA(cudaSetDevice(device_));
+  if (ipc_) {  // every rank rewrites x, then one flag-synchronised pushed step
+    const std::size_t bytes = static_cast<std::size_t>(ni_) * plane_bytes();
+    const std::size_t off = static_cast<std::size_t>(R_) * plane_bytes();
+    IMB_CUDA(cudaMemcpyAsync(static_cast<char*>(x_) + off, x_in, bytes, cudaMemcpyHostToDevice, cs_));
+    ipc_step();
+    IMB_CUDA(cudaMemcpyAsync(x_out, static_cast<char*>(x_) + off, bytes, cudaMemcpyDeviceToHost, cs_));
+    IMB_CUDA(cudaStreamSynchronize(cs_));
+    return;
+  }
   if (!static_halo_ok_) exchange_static();
   if (!(nccl_ && nccl_->nranks() > 1) && opt_.iord == 2 && tmp_[0] == nullptr && ni_ >= 4 * R_) {
     step_host_pipelined(x_in, x_out);
@@ -645,6 +663,141 @@ void Team::connect_nccl(const unsigned char* id, int nranks, int rank) {
   IMB_CUDA(cudaSetDevice(device_));
   nccl_ = std::make_unique<NcclLink>(id, nranks, rank);
   if (nranks > 1) static_halo_ok_ = static_halo_ok_ && true;
+}
+
+namespace {
+struct IpcBlob {
+  std::uint32_t magic;
+  std::int32_t device;
+  cudaIpcMemHandle_t pool;
+  cudaIpcMemHandle_t flags;
+  std::int64_t off_x, off_xn, ni, step0, plane_bytes, R;
+  std::int64_t off_st[4];
+};
+constexpr std::uint32_t kIpcMagic = 0x1b200c0du;
+static_assert(sizeof(IpcBlob) <= Team::kIpcBlobBytes, "IPC blob too large");
+}  // namespace
+
+void Team::ipc_export(unsigned char* blob) {
+  IMB_CUDA(cudaSetDevice(device_));
+  if (tmp_[0] != nullptr) throw ConfigError("IPC halo push needs the fused step kernel");
+  IpcBlob b{};
+  b.magic = kIpcMagic;
+  b.device = device_;
+  IMB_CUDA(cudaIpcGetMemHandle(&b.pool, pool_));
+  IMB_CUDA(cudaIpcGetMemHandle(&b.flags, flags_));
+  char* base = static_cast<char*>(pool_);
+  b.off_x = static_cast<char*>(x_) - base;
+  b.off_xn = static_cast<char*>(xn_) - base;
+  b.ni = ni_;
+  b.step0 = static_cast<std::int64_t>(step_count_);
+  b.plane_bytes = static_cast<std::int64_t>(plane_bytes());
+  b.R = R_;
+  for (int f = 0; f < 4; ++f) b.off_st[f] = static_cast<char*>(st_[f]) - base;
+  std::memset(blob, 0, kIpcBlobBytes);
+  std::memcpy(blob, &b, sizeof b);
+}
+
+void Team::connect_ipc(const unsigned char* left_blob, const unsigned char* right_blob,
+                       int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("bad IPC rank/size");
+  if (tmp_[0] != nullptr) throw ConfigError("IPC halo push needs the fused step kernel");
+  IMB_CUDA(cudaSetDevice(device_));
+  if (nranks == 1) return;  // periodic single slab: the self push already covers it
+  IpcBlob l, r;
+  std::memcpy(&l, left_blob, sizeof l);
+  std::memcpy(&r, right_blob, sizeof r);
+  if (l.magic != kIpcMagic || r.magic != kIpcMagic) throw ContractError("not an imb IPC blob");
+  if (l.plane_bytes != static_cast<std::int64_t>(plane_bytes()) || l.R != R_ ||
+      r.plane_bytes != static_cast<std::int64_t>(plane_bytes()) || r.R != R_)
+    throw ContractError("IPC neighbours disagree on plane size or halo radius");
+  auto open = [&](const IpcBlob& b, IpcPeer& p) {
+    void* pool = nullptr;
+    void* fl = nullptr;
+    IMB_CUDA(cudaIpcOpenMemHandle(&pool, b.pool, cudaIpcMemLazyEnablePeerAccess));
+    IMB_CUDA(cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess));
+    p.pool = static_cast<char*>(pool);
+    p.flags = static_cast<std::uint64_t*>(fl);
+    p.off_x = b.off_x;
+    p.off_xn = b.off_xn;
+    p.ni = b.ni;
+    p.step0 = b.step0;
+    for (int f = 0; f < 4; ++f) p.off_st[f] = b.off_st[f];
+    p.opened = true;
+  };
+  open(l, ipc_left_);
+  if (nranks == 2) {  // one neighbour on both sides: a handle opens once per process
+    ipc_right_ = ipc_left_;
+    ipc_right_.opened = false;
+  } else {
+    open(r, ipc_right_);
+  }
+  if (ipc_left_.step0 != static_cast<std::int64_t>(step_count_) ||
+      ipc_right_.step0 != static_cast<std::int64_t>(step_count_))
+    throw ContractError("IPC ring members must connect at the same step count");
+  ipc_ = true;
+}
+
+// One flag-synchronised step of a process ring (see group_flag_step): wait
+// until both neighbours finished step s-1, run the fused kernel whose
+// epilogue stores the edge planes into the neighbours' step-s buffers
+// (mapped over NVLink), then raise the neighbours' flag words.
+void Team::ipc_step() {
+  MemOps& ops = memops();
+  const std::uint64_t s = step_count_;
+  memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 0), s, CU_STREAM_WAIT_VALUE_GEQ),
+              "cuStreamWaitValue64");
+  memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 1), s, CU_STREAM_WAIT_VALUE_GEQ),
+              "cuStreamWaitValue64");
+  const std::size_t pb = plane_bytes(), hb = pb * static_cast<std::size_t>(R_);
+  if (!halo_fresh_ || !static_halo_ok_) {
+    // Fields were rewritten from the host (upload / reset / step_host) on
+    // every rank: post that, wait for both neighbours' posts (flag words 2
+    // and 3 count rewrite epochs), then pull their edge planes once.
+    ++post_epoch_;
+    memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_left_.flags + 3), post_epoch_,
+                          CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+    memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_right_.flags + 2), post_epoch_,
+                          CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+    memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 2), post_epoch_,
+                         CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+    memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 3), post_epoch_,
+                         CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue64");
+  }
+  if (!static_halo_ok_) {
+    for (int f = 0; f < 4; ++f) {
+      char* mine = static_cast<char*>(st_[f]);
+      IMB_CUDA(cudaMemcpyAsync(mine, ipc_left_.pool + ipc_left_.off_st[f] + pb * ipc_left_.ni, hb,
+                               cudaMemcpyDefault, cs_));
+      IMB_CUDA(cudaMemcpyAsync(mine + pb * static_cast<std::size_t>(R_ + ni_),
+                               ipc_right_.pool + ipc_right_.off_st[f] + pb * R_, hb,
+                               cudaMemcpyDefault, cs_));
+    }
+    static_halo_ok_ = true;
+  }
+  if (!halo_fresh_) {  // the neighbours' current x is the buffer they wrote in step s-1
+    char* mine = static_cast<char*>(x_);
+    const char* lsrc = static_cast<const char*>(ipc_left_.buffer(static_cast<std::int64_t>(s) - 1));
+    const char* rsrc = static_cast<const char*>(ipc_right_.buffer(static_cast<std::int64_t>(s) - 1));
+    IMB_CUDA(cudaMemcpyAsync(mine, lsrc + pb * ipc_left_.ni, hb, cudaMemcpyDefault, cs_));
+    IMB_CUDA(cudaMemcpyAsync(mine + pb * static_cast<std::size_t>(R_ + ni_), rsrc + pb * R_, hb,
+                             cudaMemcpyDefault, cs_));
+  }
+  begin_compute_window();
+  push_lo_ = ipc_left_.buffer(static_cast<std::int64_t>(s));
+  push_lo_ni_ = ipc_left_.ni;
+  push_hi_ = ipc_right_.buffer(static_cast<std::int64_t>(s));
+  swap_after_ = false;
+  compute_step();
+  swap_after_ = true;
+  end_compute_window();
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_left_.flags + 1), s + 1,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_right_.flags + 0), s + 1,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64");
+  std::swap(x_, xn_);
+  ++step_count_;
+  halo_fresh_ = true;
 }
 
 void Team::group_mark_ready() {

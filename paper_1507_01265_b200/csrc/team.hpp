@@ -59,6 +59,14 @@ class Team {
   std::uint64_t checksum();
 
   void connect_nccl(const unsigned char* id, int nranks, int rank);
+  // Multi-process halo push (one process per GPU, no NCCL): export this
+  // team's buffers as CUDA IPC handles, map the ring neighbours' and then
+  // step with the flag protocol, the step kernel storing edge planes straight
+  // into the neighbours' halos over NVLink.
+  static constexpr int kIpcBlobBytes = 512;
+  void ipc_export(unsigned char* blob);
+  void connect_ipc(const unsigned char* left_blob, const unsigned char* right_blob, int nranks,
+                   int rank);
   // In-process ring wiring (imb_group): neighbours own the adjacent slabs.
   void set_ring(Team* left, Team* right) {
     left_ = left;
@@ -139,7 +147,22 @@ class Team {
   std::int64_t push_lo_ni_ = 0;
   bool halo_fresh_ = false;
   bool swap_after_ = true;
-  std::uint64_t* flags_ = nullptr;  // [0] left neighbour's, [1] right's finished steps
+  std::uint64_t* flags_ = nullptr;  // [0]/[1] left/right neighbour's finished steps,
+                                    // [2]/[3] their host-rewrite epochs (IPC ring)
+  struct IpcPeer {
+    char* pool = nullptr;            // mapped neighbour pool (or this team's own)
+    std::uint64_t* flags = nullptr;  // mapped neighbour flag words
+    std::int64_t off_x = 0, off_xn = 0, ni = 0, step0 = 0;
+    std::int64_t off_st[4] = {0, 0, 0, 0};
+    bool opened = false;             // this process opened (and must close) it
+    void* buffer(std::int64_t s) const {  // the buffer that peer writes in step s
+      return pool + (((s - step0) % 2 == 0) ? off_xn : off_x);
+    }
+  };
+  IpcPeer ipc_left_, ipc_right_;
+  bool ipc_ = false;
+  std::uint64_t post_epoch_ = 0;  // host rewrites of x posted to the IPC neighbours
+  void ipc_step();
   std::uint64_t step_count_ = 0;    // steps taken through the group protocols
   void* out_buffer(std::uint64_t s) const;
   std::int64_t launches_ = 0;

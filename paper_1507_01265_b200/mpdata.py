@@ -131,6 +131,14 @@ class Team:
     def connect_nccl(self, uid: bytes, nranks: int, rank: int):
         check(load().imb_team_connect_nccl(self._h, uid, int(nranks), int(rank)))
 
+    def ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(512)
+        check(load().imb_team_ipc_export(self._h, buf))
+        return buf.raw
+
+    def connect_ipc(self, left: bytes, right: bytes, nranks: int, rank: int):
+        check(load().imb_team_connect_ipc(self._h, left, right, int(nranks), int(rank)))
+
 
 def ring_plan(rank: int, nranks: int, ni: int, R: int):
     """The per-step halo-swap plan the NCCL exchange executes:

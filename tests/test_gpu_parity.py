@@ -206,6 +206,32 @@ def test_contract_errors_on_gpu():
             t.upload("x", np.zeros((15, 8, 8)))
 
 
+def test_ipc_export_and_connect_contracts():
+    # The cross-process NVLink push path (imb_team_connect_ipc) needs one GPU
+    # per rank, so only its blob format and argument checks run here; its
+    # push + flag protocol is the one test_group_flag_sync_is_bit_identical
+    # exercises in-process.
+    with Team(32, 16, 64) as a, Team(32, 16, 32) as b:
+        a.init_recipe(2, 42)
+        blob = a.ipc_export()
+        assert len(blob) == 512 and int.from_bytes(blob[:4], "little") == 0x1B200C0D
+        with pytest.raises(_lib.ContractError):
+            a.connect_ipc(b"\0" * 512, b"\0" * 512, 2, 0)  # not a blob
+        with pytest.raises(_lib.ContractError):
+            a.connect_ipc(b.ipc_export(), b.ipc_export(), 2, 0)  # plane size differs
+        with pytest.raises(_lib.ContractError):
+            a.connect_ipc(blob, blob, 2, 2)  # rank out of range
+        a.connect_ipc(blob, blob, 1, 0)  # single rank: periodic self push, no mapping
+        a.run(2)
+        with Team(32, 16, 64) as c:
+            c.init_recipe(2, 42)
+            c.run(2)
+            np.testing.assert_array_equal(a.download("x"), c.download("x"))
+    with Team(32, 16, 64, Options(3, False)) as s:  # staged scheme: no fused push
+        with pytest.raises(_lib.ConfigError):
+            s.ipc_export()
+
+
 @pytest.mark.parametrize("fp64", [True, False])
 def test_full_size_properties(fp64):
     # BASELINE config 4 grid (1024x512x128): mass conservation and the
