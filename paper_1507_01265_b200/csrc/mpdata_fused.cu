@@ -48,6 +48,10 @@ __device__ unsigned long long g_phase_cycles[10];
 #define IMB_ACC(slot, a, b)
 #endif
 
+#ifndef IMB_EARLY_DONOR
+#define IMB_EARLY_DONOR 1
+#endif
+
 template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR = 1>
 struct Cfg {
   // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
@@ -59,7 +63,13 @@ struct Cfg {
   static constexpr int TJ = RR - 2 * HALO;        // output rows per tile
   static constexpr int NT = NW * 32;
   static constexpr int PLANE = RR * L;            // cells of one smem plane
-  static constexpr int NSLOT = NONOS ? 11 : 5;
+  // EARLY: the donor of plane t+3 runs in the same barrier phase as the
+  // limiter/final update of plane t (3 barriers per plane instead of 4),
+  // which takes a 4th psi^(1) slot. The STARC (register-carried psi^n star)
+  // variants keep the donor in its own phase.
+  static constexpr bool EARLY = NONOS && IMB_EARLY_DONOR && L == 128;  // l=64: measured -3.5%
+  static constexpr int NX1 = EARLY ? 4 : 3;  // psi^(1) slots
+  static constexpr int NSLOT = NONOS ? 8 + NX1 : 5;
   static constexpr std::size_t SMEM = sizeof(T) * PLANE * NSLOT;
 };
 
@@ -92,7 +102,15 @@ struct Args {
   T* push_hi;
   int lo_ni;
   int ni;
+  // L2 prefetch distance in planes (0 = off): each iteration, warp 0 issues
+  // one bulk L2 prefetch per input field for the plane `pf` planes beyond
+  // the newest one the donor stage reads, so its first touch is an L2 hit.
+  int pf;
 };
+
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes));
+}
 
 // ---- per-lane vectors of K consecutive k values ---------------------------
 template <class T, int K>
@@ -232,7 +250,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   T* s_x1 = sm;                          // 3 slots of psi^(1), by plane mod 3
-  T* s_v = sm + 3 * PL;                  // y-face pseudo-velocities
+  constexpr bool EARLY = C::EARLY && !STARC;
+  T* s_v = sm + C::NX1 * PL;             // y-face pseudo-velocities
   T* s_w = s_v + (NONOS ? 2 : 1) * PL;   // z-face pseudo-velocities
   T* s_bu = s_w + (NONOS ? 2 : 1) * PL;  // beta up,   2 slots (NONOS)
   T* s_bd = s_bu + 2 * PL;               // beta down, 2 slots (NONOS)
@@ -260,7 +279,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     gjm[rr] = (j == 0 ? m - 1 : j - 1) * L;
     gjp[rr] = (j == m - 1 ? 0 : j + 1) * L;
   }
-  auto slot3 = [](int p) { return (p + 6) % 3; };  // p >= -3
+  auto slot3 = [](int p) { return C::NX1 == 4 ? ((p + 8) & 3) : (p + 6) % 3; };  // p >= -3
   auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
   // cell group c = (row rr, segment sg): first k of this lane in the segment
   auto k0of = [&](int c) { return wcol + (c % NS) * 32 * K + lane * K; };
@@ -507,6 +526,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // pseudo-velocity between them.
   stage_donor(ib - lag);
   stage_donor(ib - lag + 1);
+  if constexpr (EARLY) stage_donor(ib - lag + 2);
   if constexpr (NONOS && STARC) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -525,12 +545,29 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   }
 
   const int tstart = NONOS ? ib - 2 : ib;
+  // Rows a plane's donor touches: region rows plus one on each side (y +- 1).
+  const int pf_j = j0 - C::HALO - 1;
+  const int pf_rows = (RR + 2 < m ? RR + 2 : m);
   for (int t = tstart; t < ie; ++t) {
     const bool emit = t >= ib;
+    if (a.pf > 0 && warp == 0 && lane < 5) {
+      const int p = t + lag + 1 + a.pf;
+      if (p <= ie + lag && p < a.ni + a.R) {
+        const T* f = lane == 0 ? a.x : lane == 1 ? a.u : lane == 2 ? a.v : lane == 3 ? a.w : a.h;
+        const T* base = f + pl(p);
+        int j = pf_j < 0 ? pf_j + m : pf_j;
+        const int first = (j + pf_rows <= m) ? pf_rows : m - j;
+        l2_prefetch(base + static_cast<long long>(j) * L, static_cast<unsigned>(first * L * sizeof(T)));
+        if (first < pf_rows)
+          l2_prefetch(base, static_cast<unsigned>((pf_rows - first) * L * sizeof(T)));
+      }
+    }
     IMB_T(0)
-    stage_donor(t + lag);  // psi^(1) of the newest plane
+    if constexpr (!EARLY) {
+      stage_donor(t + lag);  // psi^(1) of the newest plane
+      nb_sync();
+    }
     IMB_T(1)
-    nb_sync();
     IMB_T(2)
     IMB_ACC(0, 0, 1)
     IMB_ACC(1, 1, 2)
@@ -718,6 +755,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           fxc[c] = fxr;
         }
       }
+      if constexpr (EARLY) {
+        if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
+      }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         ucar[c] = ufresh[c];
@@ -852,6 +892,11 @@ int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStre
   a.o0 = static_cast<int>(fs.o0);
   a.o1 = static_cast<int>(fs.o1);
   a.plane = fs.m * fs.l;
+  static const int pf = [] {
+    const char* e = std::getenv("IMB_PF");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.pf = pf;
   kern<<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
   return 1;
 }
@@ -866,6 +911,20 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
 #ifdef IMB_FUSED_VARIANTS
       if (std::getenv("IMB_WPR2"))  // 32 warps, 2 per row, 2 x 32 cells each
         return launch_cfg<T, 128, 1, 32, 2, NONOS, false, MODE, 2>(fs, a, num_sms, st);
+      if (const char* e = std::getenv("IMB_RWV")) {  // two rows per warp, bigger tiles
+        const int v = std::atoi(e);
+        if (v == 1) return launch_cfg<T, 128, 2, 10, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (v == 2) return launch_cfg<T, 128, 2, 10, 2, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (v == 3) return launch_cfg<T, 128, 2, 8, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (v == 4) return launch_cfg<T, 128, 2, 8, 2, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (v == 7) return launch_cfg<T, 128, 2, 10, 1, NONOS, true, MODE>(fs, a, num_sms, st);
+        if (v == 8) return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, false, MODE>(fs, a, num_sms, st);
+        if (v == 9) return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, true, MODE>(fs, a, num_sms, st);
+        if constexpr (!D) {
+          if (v == 5) return launch_cfg<T, 128, 2, 16, 1, NONOS, true, MODE>(fs, a, num_sms, st);
+          if (v == 6) return launch_cfg<T, 128, 2, 12, 1, NONOS, true, MODE>(fs, a, num_sms, st);
+        }
+      }
       if (const char* e = std::getenv("IMB_NW")) {  // fewer region rows, more registers
         const int nw = std::atoi(e);
         if (nw == 14) return launch_cfg<T, 128, 1, 14, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
