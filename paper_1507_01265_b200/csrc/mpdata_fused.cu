@@ -893,8 +893,8 @@ int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStre
   a.o1 = static_cast<int>(fs.o1);
   a.plane = fs.m * fs.l;
   static const int pf = [] {
-    const char* e = std::getenv("IMB_PF");
-    return e ? std::atoi(e) : 0;
+    const char* e = std::getenv("IMB_PF");  // measured: 1 plane ahead +5% (C4 fp64)
+    return e ? std::atoi(e) : 1;
   }();
   a.pf = pf;
   kern<<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
