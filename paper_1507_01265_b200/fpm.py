@@ -268,3 +268,54 @@ def read_csv(text: str) -> SpeedFunction:
         except ValueError as e:
             raise _lib.ParseError(f"{e} (line {no})") from None
     return SpeedFunction(unit, gran, tuple(samples), label)
+
+
+# ---- 2-D speed-surface CSV: row-major in n, then m ------------
+def write_surface_csv(g: SpeedSurface) -> str:
+    rows = [f"# unit_cells={g.unit_cells} granularity={g.granularity} label={g.label}",
+            "n,m,speed,ci_halfwidth,repetitions"]
+    nm = len(g.m_values)
+    for q, s in enumerate(g.samples):
+        s = s if isinstance(s, SpeedSample) else SpeedSample(*s)
+        rows.append(f"{g.n_values[q // nm]},{s.x},{s.speed:.17g},{s.ci_halfwidth:.17g},"
+                    f"{s.repetitions}")
+    return "\n".join(rows) + "\n"
+
+
+def read_surface_csv(text: str) -> SpeedSurface:
+    lines = text.splitlines()
+    if not lines or not lines[0].startswith("# "):
+        raise _lib.ParseError("missing '# ' header (line 1)")
+    head, _, label = lines[0][2:].partition(" label=")
+    kv = dict(tok.split("=", 1) for tok in head.split() if "=" in tok)
+    try:
+        unit, gran = int(kv["unit_cells"]), int(kv["granularity"])
+    except (KeyError, ValueError) as e:
+        raise _lib.ParseError(f"bad header ({e}) (line 1)") from None
+    if len(lines) < 2 or lines[1].strip() != "n,m,speed,ci_halfwidth,repetitions":
+        raise _lib.ParseError("expected column header (line 2)")
+    ns, ms, samples = [], [], []
+    for no, line in enumerate(lines[2:], start=3):
+        if not line.strip():
+            continue
+        cols = line.split(",")
+        if len(cols) != 5:
+            raise _lib.ParseError(f"expected 5 columns (line {no})")
+        try:
+            n, m = int(cols[0]), int(cols[1])
+            samples.append(SpeedSample(m, float(cols[2]), float(cols[3]), int(cols[4])))
+        except ValueError as e:
+            raise _lib.ParseError(f"{e} (line {no})") from None
+        if not ns or ns[-1] != n:
+            if n in ns:
+                raise _lib.ParseError(f"rows not grouped by n (line {no})")
+            ns.append(n)
+        if len(ns) == 1:
+            ms.append(m)
+        else:
+            col = len(samples) - 1 - (len(ns) - 1) * len(ms)
+            if col >= len(ms) or m != ms[col]:
+                raise _lib.ParseError(f"m grid differs between n rows (line {no})")
+    if not samples or len(samples) != len(ns) * len(ms):
+        raise _lib.ParseError("surface is not a full n x m grid")
+    return SpeedSurface(unit, gran, tuple(ns), tuple(ms), tuple(samples), label)
