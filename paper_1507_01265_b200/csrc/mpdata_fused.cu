@@ -51,6 +51,9 @@ __device__ unsigned long long g_phase_cycles[10];
 #ifndef IMB_EARLY_DONOR
 #define IMB_EARLY_DONOR 1
 #endif
+#ifndef IMB_EARLY_STARC
+#define IMB_EARLY_STARC 1
+#endif
 
 template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR = 1>
 struct Cfg {
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   T* s_x1 = sm;                          // 3 slots of psi^(1), by plane mod 3
-  constexpr bool EARLY = C::EARLY && !STARC;
+  constexpr bool EARLY = C::EARLY && (!STARC || IMB_EARLY_STARC);
   T* s_v = sm + C::NX1 * PL;             // y-face pseudo-velocities
   T* s_w = s_v + (NONOS ? 2 : 1) * PL;   // z-face pseudo-velocities
   T* s_bu = s_w + (NONOS ? 2 : 1) * PL;  // beta up,   2 slots (NONOS)
@@ -305,7 +308,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #define KPS(vec, row, k0) kplus_s<L>(vec, row, k0)
 #endif
 
-  V nmx_new[NC], nmn_new[NC], nmx[NC], nmn[NC];  // psi^n star extrema (STARC)
+  // psi^n star extrema (STARC): of plane t+1 (nmx), t+2 (nmx_mid, EARLY) and
+  // the donor's newest plane (nmx_new)
+  V nmx_new[NC], nmn_new[NC], nmx[NC], nmn[NC], nmx_mid[NC], nmn_mid[NC];
 
   // P1: psi^(1) at plane p (donor cell) for all region rows.
   auto stage_donor = [&](int p) {
@@ -519,6 +524,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     for (int e = 0; e < K; ++e) {
       ucar[c].e[e] = ufresh[c].e[e] = fxc[c].e[e] = T(0);
       nmx[c].e[e] = nmn[c].e[e] = nmx_new[c].e[e] = nmn_new[c].e[e] = T(0);
+      nmx_mid[c].e[e] = nmn_mid[c].e[e] = T(0);
     }
 
   const int lag = NONOS ? 2 : 1;  // psi^(1) planes ahead of the output plane
@@ -526,12 +532,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // pseudo-velocity between them.
   stage_donor(ib - lag);
   stage_donor(ib - lag + 1);
-  if constexpr (EARLY) stage_donor(ib - lag + 2);
   if constexpr (NONOS && STARC) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       nmx[c] = nmx_new[c];
       nmn[c] = nmn_new[c];
+    }
+  }
+  if constexpr (EARLY) {
+    stage_donor(ib - lag + 2);
+    if constexpr (STARC) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        nmx_mid[c] = nmx_new[c];
+        nmn_mid[c] = nmn_new[c];
+      }
     }
   }
   __syncthreads();
@@ -761,7 +776,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         ucar[c] = ufresh[c];
-        if constexpr (STARC) {
+        if constexpr (STARC && EARLY) {
+          nmx[c] = nmx_mid[c];
+          nmn[c] = nmn_mid[c];
+          nmx_mid[c] = nmx_new[c];
+          nmn_mid[c] = nmn_new[c];
+        } else if constexpr (STARC) {
           nmx[c] = nmx_new[c];
           nmn[c] = nmn_new[c];
         }
