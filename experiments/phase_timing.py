@@ -1,4 +1,5 @@
-"""Run C4 steps with the timing build and print per-phase cycle shares."""
+"""Run C4 steps with the timing build and print per-phase cycle shares per warp
+(warp w owns region row w: rows 0,1 and 14,15 are the recomputed j-halo)."""
 import ctypes as C
 import os
 import sys
@@ -9,16 +10,20 @@ sys.path.insert(0, str(ROOT))
 from paper_1507_01265_b200 import _lib, mpdata  # noqa: E402
 lib = _lib.load()
 f = lib.imb_debug_phase_cycles
-buf = (C.c_ulonglong * 10)()
-for cfg in [(1024, 512, 128, True), (1024, 512, 128, False)]:
-    n, m, l, fp64 = cfg
+buf = (C.c_ulonglong * 320)()
+slots = [(2, "pseudo"), (3, "bar1"), (4, "beta"), (5, "bar2"), (6, "lim+fin"), (8, "donor"),
+         (7, "bar3")]
+for n, m, l, fp64 in [(1024, 512, 128, True), (1024, 512, 128, False)]:
     with mpdata.Team(n, m, l, mpdata.Options(2, True, fp64)) as t:
         t.init_recipe(2, 42)
         t.run(2)
         f(buf, 1)
         comp, wall = t.run(5)
         f(buf, 1)
-    names = ["donor", "sync1", "pseudo", "sync2", "beta", "sync3", "limit+final", "sync4"]
-    tot = sum(buf[i] for i in range(8))
-    print(f"fp64={fp64}: {n*m*l*5/wall/1e9:.2f} Gcell/s;",
-          ", ".join(f"{nm} {100*buf[i]/tot:.1f}%" for i, nm in enumerate(names)))
+    print(f"fp64={fp64}: {n*m*l*5/wall/1e9:.2f} Gcell/s (timing build)")
+    print("warp " + " ".join(f"{nm:>8}" for _, nm in slots))
+    tot = sum(buf[s * 32 + w] for s, _ in slots for w in range(16)) / 16
+    for w in range(16):
+        print(f"{w:4d} " + " ".join(f"{100 * buf[s * 32 + w] / tot:8.1f}" for s, _ in slots))
+    print("all  " + " ".join(f"{100 * sum(buf[s * 32 + w] for w in range(16)) / 16 / tot:8.1f}"
+                             for s, _ in slots))

@@ -39,10 +39,11 @@ constexpr unsigned kFull = 0xffffffffu;
 
 #ifdef IMB_PHASE_TIMING
 // Debug-only per-phase cycle accounting (lane 0 of every warp), off in the product build.
-__device__ unsigned long long g_phase_cycles[10];
+__device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_T(i) const long long imb_tp##i = clock64();
 #define IMB_ACC(slot, a, b) \
-  if (lane == 0) atomicAdd(&g_phase_cycles[slot], static_cast<unsigned long long>(imb_tp##b - imb_tp##a));
+  if (lane == 0)          \
+    atomicAdd(&g_phase_cycles[(slot) * 32 + warp], static_cast<unsigned long long>(imb_tp##b - imb_tp##a));
 #else
 #define IMB_T(i)
 #define IMB_ACC(slot, a, b)
@@ -770,6 +771,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           fxc[c] = fxr;
         }
       }
+      IMB_T(9)
       if constexpr (EARLY) {
         if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
       }
@@ -789,7 +791,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       IMB_T(7)
       nb_sync();
       IMB_T(8)
-      IMB_ACC(6, 6, 7)
+      IMB_ACC(6, 6, 9)
+      IMB_ACC(8, 9, 7)
       IMB_ACC(7, 7, 8)
     } else {
       // Plain IORD=2: pseudo-velocities of plane t, then the final update.
@@ -970,7 +973,7 @@ bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool) 
 extern "C" int imb_debug_phase_cycles(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
   if (reset) {
-    unsigned long long z[10] = {};
+    unsigned long long z[10 * 32] = {};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   }
   return 0;
