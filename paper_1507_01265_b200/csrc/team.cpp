@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -215,6 +216,8 @@ Team::~Team() {
   if (ups_) cudaStreamDestroy(ups_);
   if (dns_) cudaStreamDestroy(dns_);
   for (cudaEvent_t e : ev_pipe_) cudaEventDestroy(e);
+  for (cudaGraphExec_t g : graph_)
+    if (g) cudaGraphExecDestroy(g);
   if (pool_) cudaFree(pool_);
   if (flags_) cudaFree(flags_);
   for (IpcPeer* p : {&ipc_left_, &ipc_right_})
@@ -500,6 +503,44 @@ void Team::step_overlapped() {
   std::swap(x_, xn_);
 }
 
+// Two self-pushing fused steps as one graph replay (x -> xn -> x). Captured on
+// first use for each starting buffer; returns false if capture is unavailable
+// (the caller then launches the step directly).
+bool Team::graph_step_pair() {
+  const int slot = (x_ == graph_x_[0]) ? 0 : (x_ == graph_x_[1]) ? 1 : (graph_x_[0] ? 1 : 0);
+  if (graph_[slot] == nullptr || graph_x_[slot] != x_) {
+    if (graph_[slot]) IMB_CUDA(cudaGraphExecDestroy(graph_[slot]));
+    graph_[slot] = nullptr;
+    void* x0 = x_;
+    const std::int64_t l0 = launches_;
+    IMB_CUDA(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < 2; ++k) {
+      push_lo_ = push_hi_ = xn_;
+      push_lo_ni_ = ni_;
+      compute_step();  // swaps x_ and xn_
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cs_, &g);
+    graph_launches_ = launches_ - l0;
+    launches_ = l0;
+    if (e != cudaSuccess || g == nullptr) {  // nothing ran (x_ is back to x0)
+      cudaGetLastError();
+      return false;
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&graph_[slot], g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      graph_[slot] = nullptr;
+      return false;
+    }
+    graph_x_[slot] = x0;
+  }
+  IMB_CUDA(cudaGraphLaunch(graph_[slot], cs_));
+  launches_ += graph_launches_;
+  return true;
+}
+
 void Team::run(int steps, double* compute_s, double* wall_s) {
   if (steps < 0) throw ContractError("steps must be >= 0");
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
@@ -513,6 +554,11 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   ev_used_ = 0;
   const bool overlap = multi && opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
   const bool self_push = !multi && !ipc_ && tmp_[0] == nullptr;
+  static const bool graphs_on = [] {
+    const char* e = std::getenv("IMB_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  const bool use_graph = graphs_on && self_push && steps >= 4;
   for (int s = 0; s < steps; ++s) {
     if (ipc_) {
       ipc_step();
@@ -526,6 +572,15 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
       // Periodic single slab: the kernel's epilogue writes the edge planes
       // into the opposite halos of its own output, so after the first step
       // no exchange is needed at all.
+      if (halo_fresh_ && use_graph && s + 2 <= steps) {
+        begin_compute_window();
+        if (graph_step_pair()) {
+          end_compute_window();
+          ++s;
+          continue;
+        }
+        end_compute_window();
+      }
       if (!halo_fresh_) exchange_x_self(x_);
       push_lo_ = push_hi_ = xn_;
       push_lo_ni_ = ni_;

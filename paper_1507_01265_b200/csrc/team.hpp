@@ -166,6 +166,12 @@ class Team {
   std::uint64_t step_count_ = 0;    // steps taken through the group protocols
   void* out_buffer(std::uint64_t s) const;
   std::int64_t launches_ = 0;
+  // Periodic single slab: two fused steps (x -> xn -> x) captured as one CUDA
+  // graph per starting buffer, replayed to cut per-step launch overhead.
+  cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+  void* graph_x_[2] = {nullptr, nullptr};
+  std::int64_t graph_launches_ = 0;  // kernels per replay
+  bool graph_step_pair();
   Team* left_ = nullptr;
   Team* right_ = nullptr;
   std::unique_ptr<NcclLink> nccl_;
