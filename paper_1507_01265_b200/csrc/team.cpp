@@ -552,7 +552,16 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   IMB_CUDA(cudaEventRecord(t0, cs_));
   if (!static_halo_ok_) exchange_static();
   ev_used_ = 0;
-  const bool overlap = multi && opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
+  // Hiding the exchange behind the interior costs two extra launches for the
+  // 2R boundary planes; each streams R planes plus the warm-up on one block
+  // per SM (~7 plane-times, ~75 us at C4 rows), while an NVLink exchange of
+  // 2R planes takes ~20 us. So by default the exchange runs first and one
+  // launch covers the slab; IMB_OVERLAP=1 selects the overlapped schedule.
+  static const bool overlap_on = [] {
+    const char* e = std::getenv("IMB_OVERLAP");
+    return e && e[0] == '1';
+  }();
+  const bool overlap = overlap_on && multi && opt_.iord == 2 && tmp_[0] == nullptr && ni_ > 2 * R_;
   const bool self_push = !multi && !ipc_ && tmp_[0] == nullptr;
   static const bool graphs_on = [] {
     const char* e = std::getenv("IMB_GRAPH");
