@@ -232,6 +232,32 @@ def test_ipc_export_and_connect_contracts():
             s.ipc_export()
 
 
+def _mass(h, x):
+    # plane-chunked pairwise sums, combined exactly (fsum): no 2 GB temporaries
+    import math
+    return math.fsum(float(np.sum(h[i:i + 64].astype(np.float64) * x[i:i + 64]))
+                     for i in range(0, x.shape[0], 64))
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+def test_full_size_properties_c5(fp64):
+    # BASELINE config 5 grid (2048x1024x128, IORD=3 + limiter): the largest
+    # single-GPU problem; mass conservation and bounds after 2 steps.
+    opts = Options(3, True, fp64)
+    with Team(2048, 1024, 128, opts) as t:
+        t.init_recipe(2, 42)
+        x0 = t.download("x")
+        h = t.download("h")
+        m0 = _mass(h, x0.astype(np.float64))
+        lo, hi = float(x0.min()), float(x0.max())
+        del x0
+        t.run(2)
+        x = t.download("x").astype(np.float64)
+    tol = 1e-12 if fp64 else 1e-5
+    assert abs(_mass(h, x) - m0) <= tol * m0
+    assert x.min() >= lo - 1e-3 and x.max() <= hi + 1e-3
+
+
 @pytest.mark.parametrize("fp64", [True, False])
 def test_full_size_properties(fp64):
     # BASELINE config 4 grid (1024x512x128): mass conservation and the
