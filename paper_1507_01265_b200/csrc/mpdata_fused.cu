@@ -27,6 +27,11 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "mpdata_kernels.cuh"
 #include "mpdata_math.cuh"
@@ -88,7 +93,7 @@ struct Args {
   int m;            // rows (j extent)
   int R;            // halo planes of the padded slab
   int ntj;          // j tiles
-  int nseg;         // i segments
+  int kseg, lseg;   // per j-tile: kseg segments of lseg planes, then one remainder block
   int o0, o1;       // output plane range (interior coordinates)
   long long plane;  // m * l
   // IORD=3 split (MODE 1 writes, MODE 2 reads): bounds and limited velocities
@@ -260,11 +265,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   T* s_bu = s_w + (NONOS ? 2 : 1) * PL;  // beta up,   2 slots (NONOS)
   T* s_bd = s_bu + 2 * PL;               // beta down, 2 slots (NONOS)
 
-  const int tile = blockIdx.x % a.ntj;
-  const int seg = blockIdx.x / a.ntj;
-  const int span = a.o1 - a.o0;
-  const int ib = a.o0 + static_cast<int>((static_cast<long long>(span) * seg) / a.nseg);
-  const int ie = a.o0 + static_cast<int>((static_cast<long long>(span) * (seg + 1)) / a.nseg);
+  // Blocks [0, ntj*kseg): segment blockIdx/ntj of tile blockIdx%ntj, lseg
+  // planes each; then one block per tile for the remaining planes (if any).
+  // Issued longest first, the short remainder blocks fill the SMs that the
+  // long ones leave idle (see plan_grid).
+  const int nbig = a.ntj * a.kseg;
+  const bool big = static_cast<int>(blockIdx.x) < nbig;
+  const int tile = big ? blockIdx.x % a.ntj : blockIdx.x - nbig;
+  const int ib = a.o0 + (big ? static_cast<int>(blockIdx.x / a.ntj) * a.lseg : a.kseg * a.lseg);
+  const int ie = big ? ib + a.lseg : a.o1;
   if (ib >= ie) return;
   const int j0 = tile * C::TJ;
   const int m = a.m;
@@ -872,24 +881,50 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 }
 
 struct Plan {
-  int ntj, nseg;
+  int ntj, kseg, lseg, blocks;
 };
 
-// Choose the i-segmentation: minimise waves x (planes per segment + warm-up).
+// Choose the i-segmentation of every j-tile: kseg segments of lseg planes
+// plus one remainder segment, blocks issued longest first. Each candidate
+// lseg is scored by simulating the block scheduler (a block goes to the
+// resident slot that frees first; a block costs its planes + the warm-up);
+// the smallest makespan wins, then the fewest blocks. Uniform splits are the
+// candidates with no remainder. Plans are cached per shape.
 Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int warm) {
-  Plan best{static_cast<int>((m + tj - 1) / tj), 1};
-  double best_cost = 1e300;
-  for (int nseg = 1; nseg <= planes; ++nseg) {
-    const long long blocks = static_cast<long long>(best.ntj) * nseg;
-    if (blocks > INT_MAX / 2) break;
-    const long long waves = (blocks + resident - 1) / resident;
-    const long long seg = (planes + nseg - 1) / nseg;
-    const double cost = static_cast<double>(waves) * static_cast<double>(seg + warm);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best.nseg = nseg;
+  static std::mutex mu;
+  static std::map<std::tuple<std::int64_t, int, std::int64_t, int, int>, Plan> cache;
+  const auto key = std::make_tuple(m, tj, planes, resident, warm);
+  std::lock_guard<std::mutex> lock(mu);
+  if (auto it = cache.find(key); it != cache.end()) return it->second;
+  const int ntj = static_cast<int>((m + tj - 1) / tj);
+  Plan best{ntj, 1, static_cast<int>(planes), ntj};
+  long long best_span = LLONG_MAX;
+  const long long min_len = std::max<long long>(1, planes / 256);
+  std::vector<long long> slot;
+  for (long long len = planes; len >= min_len; --len) {
+    const long long k = planes / len, rem = planes - k * len;
+    const long long blocks = ntj * k + (rem > 0 ? ntj : 0);
+    if (blocks > 16LL * resident || blocks > INT_MAX / 2) continue;
+    // longest-first list scheduling on `resident` slots
+    slot.assign(static_cast<std::size_t>(std::min<long long>(resident, blocks)), 0);
+    std::make_heap(slot.begin(), slot.end(), std::greater<long long>());
+    long long makespan = 0;
+    auto issue = [&](long long count, long long cost) {
+      for (long long b = 0; b < count; ++b) {
+        std::pop_heap(slot.begin(), slot.end(), std::greater<long long>());
+        slot.back() += cost;
+        makespan = std::max(makespan, slot.back());
+        std::push_heap(slot.begin(), slot.end(), std::greater<long long>());
+      }
+    };
+    issue(ntj * k, len + warm);
+    if (rem > 0) issue(ntj, rem + warm);
+    if (makespan < best_span || (makespan == best_span && blocks < best.blocks)) {
+      best_span = makespan;
+      best = Plan{ntj, static_cast<int>(k), static_cast<int>(len), static_cast<int>(blocks)};
     }
   }
+  cache.emplace(key, best);
   return best;
 }
 
@@ -911,7 +946,8 @@ int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStre
   a.m = static_cast<int>(fs.m);
   a.R = static_cast<int>(fs.R);
   a.ntj = p.ntj;
-  a.nseg = p.nseg;
+  a.kseg = p.kseg;
+  a.lseg = p.lseg;
   a.o0 = static_cast<int>(fs.o0);
   a.o1 = static_cast<int>(fs.o1);
   a.plane = fs.m * fs.l;
@@ -920,7 +956,7 @@ int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStre
     return e ? std::atoi(e) : 1;
   }();
   a.pf = pf;
-  kern<<<p.ntj * p.nseg, C::NT, C::SMEM, st>>>(a);
+  kern<<<p.blocks, C::NT, C::SMEM, st>>>(a);
   return 1;
 }
 
@@ -988,7 +1024,7 @@ int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T*
                  const T* w, const T* h, T* out, int num_sms, cudaStream_t st,
                  const HaloPush<T>& push) {
   if (iord != 2) return 0;
-  Args<T> a{x, u, v, w, h, out, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
+  Args<T> a{x, u, v, w, h, out, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
             push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
   return nonos ? dispatch_l<T, true, 0>(fs, a, num_sms, st)
                : dispatch_l<T, false, 0>(fs, a, num_sms, st);
@@ -1003,10 +1039,10 @@ int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, cons
   FusedShape f1 = fs;
   f1.o0 = fs.o0 - 2;
   f1.o1 = fs.o1 + 2;
-  Args<T> a1{x, u, v, w, h, x2, 0, 0, 0, 0, 0, 0, 0, mx, mn, u2, v2, w2,
+  Args<T> a1{x, u, v, w, h, x2, 0, 0, 0, 0, 0, 0, 0, 0, mx, mn, u2, v2, w2,
              nullptr, nullptr, 0, static_cast<int>(fs.ni)};
   int n = dispatch_l<T, true, 1>(f1, a1, num_sms, st);
-  Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr,
+  Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr,
              push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
   n += dispatch_l<T, true, 2>(fs, a2, num_sms, st);
   return n;
