@@ -7,8 +7,10 @@
 One "step" is one MPDATA time step over the whole grid. The default workload
 is BASELINE config 4 (1024x512x128 fp64, IORD=2, nonoscillatory, periodic),
 the configuration the metric is quoted on at 1/2/4/8 GPUs; at N>1 (torchrun,
-one process per GPU) the grid is split into i-slabs (even, or --shares) with
-a per-step NCCL halo exchange inside the C-ABI run call (strong scaling).
+one process per GPU) the grid is split into i-slabs (even, or --shares) and
+the step kernel pushes its edge planes into the CUDA-IPC-mapped neighbour
+halos over NVLink, ordered by device flag words (--halo ipc, the default;
+--halo nccl or a failed mapping uses a per-step NCCL exchange) — strong scaling.
 
 ``value`` = interior cell-updates of all ranks / max-over-ranks device time of
 K steps (CUDA events inside the library, exchange included). ``e2e`` = the
@@ -166,9 +168,13 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--shares", default="", help="comma-separated slab shares (N>1)")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "ipc"],
-                    help="N>1 halo exchange: NCCL send/recv, or the step kernel pushing "
-                         "edge planes into CUDA-IPC-mapped neighbour halos")
+    ap.add_argument("--halo", default="ipc", choices=["nccl", "ipc"],
+                    help="N>1 halo exchange: the step kernel pushing its edge planes into "
+                         "the CUDA-IPC-mapped neighbour halos over NVLink (default; falls "
+                         "back to NCCL if the mapping fails), or NCCL send/recv")
+    ap.add_argument("--one-device", action="store_true",
+                    help="testing only: every rank on GPU 0 (exercises the N>1 code path "
+                         "on a 1-GPU box; the numbers are not a scaling result)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -187,6 +193,8 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo", rank=rank, world_size=world)
+    if args.one_device:
+        local = 0
     torch.cuda.set_device(local)
     if args.shares:
         shares = [int(s) for s in args.shares.split(",")]
@@ -197,12 +205,27 @@ def main():
     opts = mpdata.Options(iord=iord, nonos=nonos, fp64=fp64)
     team = mpdata.Team(n, m, l, opts, device=local, i0=i0, ni=shares[rank])
     team.init_recipe(recipe, 42)
-    if world > 1 and args.halo == "ipc":
+    halo = args.halo
+    if world > 1 and halo == "ipc":
         blobs = [None] * world
         dist.all_gather_object(blobs, team.ipc_export())
-        team.connect_ipc(blobs[(rank - 1) % world], blobs[(rank + 1) % world], world, rank)
+        err = ""
+        try:
+            team.connect_ipc(blobs[(rank - 1) % world], blobs[(rank + 1) % world], world, rank)
+        except mpdata._lib.ImbError as e:
+            err = str(e)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if any(errs):  # every rank falls back together
+            if rank == 0:
+                print(f"ipc halo push unavailable ({next(e for e in errs if e)}); using NCCL",
+                      file=sys.stderr)
+            team.close()
+            team = mpdata.Team(n, m, l, opts, device=local, i0=i0, ni=shares[rank])
+            team.init_recipe(recipe, 42)
+            halo = "nccl"
         dist.barrier()
-    elif world > 1:
+    if world > 1 and halo == "nccl":
         uid = [mpdata.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         team.connect_nccl(uid[0], world, rank)
@@ -271,7 +294,7 @@ def main():
         "dtype": "f64" if fp64 else "f32", "data": "synthetic (seeded BASELINE recipe, device-generated)",
         "config": {"workload": desc, "grid": [n, m, l], "iord": iord, "nonos": nonos,
                    "boundary": "periodic", "shares": shares,
-                   "parallelism": f"slab{world}" + (f" {args.halo}-halo" if world > 1 else ""),
+                   "parallelism": f"slab{world}" + (f" {halo}-halo" if world > 1 else ""),
                    "l2": f"inputs larger than L2 (5 fields x {cells * elem >> 20} MiB)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": local_cells * elem, "d2h_bytes_per_step": local_cells * elem,

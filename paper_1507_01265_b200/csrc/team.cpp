@@ -799,6 +799,20 @@ void Team::connect_ipc(const unsigned char* left_blob, const unsigned char* righ
   if (ipc_left_.step0 != static_cast<std::int64_t>(step_count_) ||
       ipc_right_.step0 != static_cast<std::int64_t>(step_count_))
     throw ContractError("IPC ring members must connect at the same step count");
+  // Probe now, while no rank steps, that this stream can write the mapped
+  // flag words (peer memory over NVLink): rewrite the values they already
+  // hold (only this rank writes the words that describe it), so a missing
+  // capability fails here instead of leaving a neighbour waiting mid-step.
+  MemOps& ops = memops();
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_left_.flags + 1), step_count_,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64 (peer)");
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_right_.flags + 0), step_count_,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64 (peer)");
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_left_.flags + 3), post_epoch_,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64 (peer)");
+  memop_check(ops.write(cs_, reinterpret_cast<CUdeviceptr>(ipc_right_.flags + 2), post_epoch_,
+                        CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue64 (peer)");
+  IMB_CUDA(cudaStreamSynchronize(cs_));
   ipc_ = true;
 }
 

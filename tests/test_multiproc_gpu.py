@@ -1,0 +1,36 @@
+"""Multi-process paths on one GPU (every rank on device 0): the CUDA-IPC halo
+push ring must be bit-identical to a single slab, and bench.py's N>1 code
+path must produce its JSON line. Each launch runs under a hard timeout."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def torchrun(nproc, port, *args, timeout=180):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(nproc), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), *map(str, args)]
+    return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_ring_processes_bit_identical(world):
+    r = torchrun(world, 29610 + world, "tests/mp/ipc_ring.py")
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"ipc ring world={world}: bit-identical" in r.stdout
+
+
+def test_bench_two_ranks_json_line():
+    r = torchrun(2, 29620, "bench.py", "--gpus", 2, "--one-device", "--config", "c2",
+                 "--steps", 3, "--warmup", 3, "--e2e-steps", 1, "--no-cpu-baseline")
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["config"]["parallelism"] == "slab2 ipc-halo"
+    assert line["e2e"]["value"] > 0
