@@ -115,7 +115,12 @@ int imb_team_connect_nccl(imb_team* t, const unsigned char id[IMB_NCCL_ID_BYTES]
  * on device flag words (cuStreamWaitValue64), the step kernel stores its edge
  * planes straight into the neighbours' halos, and the rank raises the
  * neighbours' flags (cuStreamWriteValue64). All ranks must connect at the
- * same step count and then step in lockstep. */
+ * same step count and then step in lockstep; host rewrites of x (upload,
+ * reset, step_host) must also happen on every rank. Connecting probes the
+ * peer flag writes, so an unsupported mapping fails there (status 20)
+ * before any rank steps. Synchronise all ranks (any control-plane barrier
+ * after their last run) before destroying a connected team: the neighbours'
+ * kernels write into its buffers. */
 enum { IMB_IPC_BLOB_BYTES = 512 };
 int imb_team_ipc_export(imb_team* t, unsigned char blob[IMB_IPC_BLOB_BYTES]);
 int imb_team_connect_ipc(imb_team* t, const unsigned char left[IMB_IPC_BLOB_BYTES],
