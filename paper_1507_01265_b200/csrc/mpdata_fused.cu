@@ -987,6 +987,8 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
         if (v == 10) return launch_cfg<T, 128, 1, 16, 1, NONOS, false, MODE>(fs, a, num_sms, st);
         if (v == 11) return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE>(fs, a, num_sms, st);
         if (v == 12) return launch_cfg<T, 128, 1, 16, 4, NONOS, false, MODE>(fs, a, num_sms, st);
+        if (v == 13) return launch_cfg<T, 128, 1, 16, 2, NONOS, true, MODE>(fs, a, num_sms, st);
+        if (v == 14) return launch_cfg<T, 128, 1, 16, 2, NONOS, false, MODE>(fs, a, num_sms, st);
         if constexpr (!D) {
           if (v == 5) return launch_cfg<T, 128, 2, 16, 1, NONOS, true, MODE>(fs, a, num_sms, st);
           if (v == 6) return launch_cfg<T, 128, 2, 12, 1, NONOS, true, MODE>(fs, a, num_sms, st);
