@@ -51,7 +51,8 @@ def test_config2_parity(orc):
 
 
 @pytest.mark.parametrize("fp64", [True, False])
-@pytest.mark.parametrize("iord,nonos", [(1, False), (2, False), (2, True), (3, True), (3, False)])
+@pytest.mark.parametrize("iord,nonos", [(1, False), (2, False), (2, True), (3, True), (3, False),
+                                        (4, True), (4, False)])
 @pytest.mark.parametrize("recipe", [0, 2])
 def test_scheme_matrix_parity(orc, fp64, iord, nonos, recipe):
     opts = Options(iord=iord, nonos=nonos, fp64=fp64)
