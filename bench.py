@@ -295,7 +295,10 @@ def main():
         "config": {"workload": desc, "grid": [n, m, l], "iord": iord, "nonos": nonos,
                    "boundary": "periodic", "shares": shares,
                    "parallelism": f"slab{world}" + (f" {halo}-halo" if world > 1 else ""),
-                   "l2": f"inputs larger than L2 (5 fields x {cells * elem >> 20} MiB)"},
+                   "l2": f"inputs larger than L2 (5 fields x {cells * elem >> 20} MiB)",
+                   # halo planes each GPU sends per step, per direction
+                   "halo_bytes_per_gpu_per_step": (2 * mpdata.step_radius(opts) * m * l * elem
+                                                   if world > 1 else 0)},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": local_cells * elem, "d2h_bytes_per_step": local_cells * elem,
                 "path": "imb_team_step_host (pinned host x in, step incl. halo exchange, x out)"},
