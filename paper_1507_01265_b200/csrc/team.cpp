@@ -724,9 +724,9 @@ std::uint64_t Team::checksum() {
 
 void Team::connect_nccl(const unsigned char* id, int nranks, int rank) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("bad NCCL rank/size");
+  if (left_ || right_ || ipc_ || nccl_) throw ContractError("team is already part of a ring");
   IMB_CUDA(cudaSetDevice(device_));
   nccl_ = std::make_unique<NcclLink>(id, nranks, rank);
-  if (nranks > 1) static_halo_ok_ = static_halo_ok_ && true;
 }
 
 namespace {
@@ -765,6 +765,7 @@ void Team::ipc_export(unsigned char* blob) {
 void Team::connect_ipc(const unsigned char* left_blob, const unsigned char* right_blob,
                        int nranks, int rank) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("bad IPC rank/size");
+  if (left_ || right_ || ipc_ || nccl_) throw ContractError("team is already part of a ring");
   if (tmp_[0] != nullptr) throw ConfigError("IPC halo push needs the fused step kernel");
   IMB_CUDA(cudaSetDevice(device_));
   if (nranks == 1) return;  // periodic single slab: the self push already covers it
