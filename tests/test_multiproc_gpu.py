@@ -2,6 +2,8 @@
 push ring must be bit-identical to a single slab, and bench.py's N>1 code
 path must produce its JSON line. Each launch runs under a hard timeout."""
 import json
+import os
+import signal
 import subprocess
 import sys
 from pathlib import Path
@@ -13,10 +15,20 @@ ROOT = Path(__file__).resolve().parents[1]
 
 
 def torchrun(nproc, port, *args, timeout=180):
+    """Run in its own process group; on timeout the whole group (launcher and
+    every rank) is killed so no rank is left holding the GPU."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
            "--nproc-per-node", str(nproc), "--master-addr", "127.0.0.1",
            "--master-port", str(port), *map(str, args)]
-    return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    p = subprocess.Popen(cmd, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                         text=True, start_new_session=True)
+    try:
+        out, err = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, err = p.communicate()
+        pytest.fail(f"{cmd} timed out after {timeout} s\n{out[-2000:]}\n{err[-2000:]}")
+    return subprocess.CompletedProcess(cmd, p.returncode, out, err)
 
 
 @pytest.mark.parametrize("world", [2, 3])
