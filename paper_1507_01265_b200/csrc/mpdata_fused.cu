@@ -35,12 +35,11 @@
 
 #include "mpdata_kernels.cuh"
 #include "mpdata_math.cuh"
+#include "mpdata_vec.cuh"
 
 namespace imb::dev {
 
 namespace {
-
-constexpr unsigned kFull = 0xffffffffu;
 
 #ifdef IMB_PHASE_TIMING
 // Debug-only per-phase cycle accounting (lane 0 of every warp), off in the product build.
@@ -116,136 +115,6 @@ struct Args {
   // the newest one the donor stage reads, so its first touch is an L2 hit.
   int pf;
 };
-
-__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes));
-}
-
-// ---- per-lane vectors of K consecutive k values ---------------------------
-template <class T, int K>
-struct Vec {
-  T e[K];
-};
-
-template <class T, int K>
-__device__ __forceinline__ Vec<T, K> vload(const T* p) {  // global, read-only path
-  Vec<T, K> r;
-  if constexpr (sizeof(T) == 8 && K == 4) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
-  } else if constexpr (sizeof(T) == 8 && K == 2) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    r.e[0] = a.x; r.e[1] = a.y;
-  } else if constexpr (sizeof(T) == 4 && K == 4) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = a.z; r.e[3] = a.w;
-  } else if constexpr (sizeof(T) == 4 && K == 2) {
-    const float2 a = __ldg(reinterpret_cast<const float2*>(p));
-    r.e[0] = a.x; r.e[1] = a.y;
-  } else {
-    r.e[0] = __ldg(p);
-  }
-  return r;
-}
-
-template <class T, int K>
-__device__ __forceinline__ Vec<T, K> sload(const T* p) {  // shared
-  Vec<T, K> r;
-  if constexpr (sizeof(T) == 8 && K == 4) {
-    const double2 a = reinterpret_cast<const double2*>(p)[0];
-    const double2 b = reinterpret_cast<const double2*>(p)[1];
-    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
-  } else if constexpr (sizeof(T) == 8 && K == 2) {
-    const double2 a = reinterpret_cast<const double2*>(p)[0];
-    r.e[0] = a.x; r.e[1] = a.y;
-  } else if constexpr (sizeof(T) == 4 && K == 4) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = a.z; r.e[3] = a.w;
-  } else if constexpr (sizeof(T) == 4 && K == 2) {
-    const float2 a = reinterpret_cast<const float2*>(p)[0];
-    r.e[0] = a.x; r.e[1] = a.y;
-  } else {
-    r.e[0] = p[0];
-  }
-  return r;
-}
-
-template <class T, int K>
-__device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or global
-  if constexpr (sizeof(T) == 8 && K == 4) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v.e[2], v.e[3]);
-  } else if constexpr (sizeof(T) == 8 && K == 2) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
-  } else if constexpr (sizeof(T) == 4 && K == 4) {
-    reinterpret_cast<float4*>(p)[0] = make_float4(v.e[0], v.e[1], v.e[2], v.e[3]);
-  } else if constexpr (sizeof(T) == 4 && K == 2) {
-    reinterpret_cast<float2*>(p)[0] = make_float2(v.e[0], v.e[1]);
-  } else {
-    p[0] = v.e[0];
-  }
-}
-
-// Value at k-1 / k+1 of a lane vector. The warp holds NS consecutive
-// segments of 32*K cells per row; inside a segment the neighbour is one
-// shuffle away, and with NS == 1 the shuffle also closes the periodic k wrap.
-// With NS > 1 the segment-edge lane reloads its single neighbour from the
-// vector's source row (global read-only path when G, shared memory else).
-template <int L, int NS, bool G, class T, int K>
-__device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, const T* row, int k0, int lane) {
-  Vec<T, K> r;
-  r.e[0] = __shfl_sync(kFull, a.e[K - 1], (lane + 31) & 31);
-  if constexpr (NS > 1) {
-    if (lane == 0) {
-      const T* p = row + (k0 == 0 ? L - 1 : k0 - 1);
-      r.e[0] = G ? __ldg(p) : *p;
-    }
-  }
-#pragma unroll
-  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
-  return r;
-}
-template <int L, int NS, bool G, class T, int K>
-__device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, const T* row, int k0, int lane) {
-  Vec<T, K> r;
-  r.e[K - 1] = __shfl_sync(kFull, a.e[0], (lane + 1) & 31);
-  if constexpr (NS > 1) {
-    if (lane == 31) {
-      const T* p = row + (k0 + K == L ? 0 : k0 + K);
-      r.e[K - 1] = G ? __ldg(p) : *p;
-    }
-  }
-#pragma unroll
-  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
-  return r;
-}
-// k-1 / k+1 of a vector held in shared memory: the single out-of-vector
-// element is read back from the row (periodic wrap in the address), so no
-// shuffle and no edge-lane special case.
-template <int L, class T, int K>
-__device__ __forceinline__ Vec<T, K> kminus_s(const Vec<T, K>& a, const T* row, int k0) {
-  Vec<T, K> r;
-  r.e[0] = row[k0 == 0 ? L - 1 : k0 - 1];
-#pragma unroll
-  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
-  return r;
-}
-template <int L, class T, int K>
-__device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* row, int k0) {
-  Vec<T, K> r;
-  r.e[K - 1] = row[k0 + K == L ? 0 : k0 + K];
-#pragma unroll
-  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
-  return r;
-}
-template <class T, int K>
-__device__ __forceinline__ Vec<T, K> vabs(const Vec<T, K>& a) {
-  Vec<T, K> r;
-#pragma unroll
-  for (int e = 0; e < K; ++e) r.e[e] = fabs(a.e[e]);
-  return r;
-}
 
 // MODE 0: one IORD=2 step. MODE 1: donor + first corrective pass of an
 // IORD=3 step, additionally writing the pass's limited velocities and 7-point
