@@ -749,9 +749,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #undef KPS
 }
 
-struct Plan {
-  int ntj, kseg, lseg, blocks;
-};
+}  // namespace
 
 // Choose the i-segmentation of every j-tile: kseg segments of lseg planes
 // plus one remainder segment, blocks issued longest first. Each candidate
@@ -796,6 +794,8 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   cache.emplace(key, best);
   return best;
 }
+
+namespace {
 
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, int WPR = 1>
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {

@@ -56,6 +56,13 @@ struct HaloPush {
   std::int64_t lo_ni = 0;   // left neighbour's interior planes
   T* hi = nullptr;          // right neighbour's output buffer
 };
+// Segmentation of a streaming launch: per j-tile of `tj` rows, kseg
+// segments of lseg planes plus one remainder segment (blocks issued longest
+// first); chosen by simulating the block scheduler (mpdata_fused.cu).
+struct Plan {
+  int ntj, kseg, lseg, blocks;
+};
+Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int warm);
 // True when the fused kernel supports this (iord, nonos, m, l) combination.
 bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool fp64);
 template <class T>
