@@ -866,6 +866,7 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
       if (const char* e = std::getenv("IMB_NW")) {  // fewer region rows, more registers
         const int nw = std::atoi(e);
         if (nw == 14) return launch_cfg<T, 128, 1, 14, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+        if (nw == 15) return launch_cfg<T, 128, 1, 15, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
         if (nw == 12) return launch_cfg<T, 128, 1, 12, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
         if (nw == 20) return launch_cfg<T, 128, 1, 20, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
       }
