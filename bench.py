@@ -166,7 +166,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--shares", default="", help="comma-separated slab shares (N>1)")
+    ap.add_argument("--shares", default="",
+                    help="N>1 slab shares: comma-separated planes, or a speed-function CSV "
+                         "(cli measure output) to split with the FPM partitioner "
+                         "(Algorithm 1 for even N, the exact DP otherwise)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--halo", default="ipc", choices=["nccl", "ipc"],
                     help="N>1 halo exchange: the step kernel pushing its edge planes into "
@@ -196,7 +199,13 @@ def main():
     if args.one_device:
         local = 0
     torch.cuda.set_device(local)
-    if args.shares:
+    if args.shares.endswith(".csv"):
+        from paper_1507_01265_b200 import fpm
+        model = fpm.read_csv(Path(args.shares).read_text())
+        pr = fpm.PartitionProblem(n, world, model)
+        part = fpm.partition_paired(pr) if world % 2 == 0 else fpm.partition_general(pr)
+        shares = list(part.shares)
+    elif args.shares:
         shares = [int(s) for s in args.shares.split(",")]
     else:
         shares = [n // world + (1 if r < n % world else 0) for r in range(world)]
