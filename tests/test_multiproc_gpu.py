@@ -46,3 +46,15 @@ def test_bench_two_ranks_json_line():
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["parallelism"] == "slab2 ipc-halo"
     assert line["e2e"]["value"] > 0
+
+
+def test_bench_fpm_shares_from_speed_function():
+    # --shares <speed-function CSV>: Algorithm 1 over the ranks (an even split
+    # here: the measured B200 speed function satisfies Eq. (1)).
+    model = ROOT / "profiles" / "r01_cli_c4" / "speed_avg.csv"
+    r = torchrun(2, 29621, "bench.py", "--gpus", 2, "--one-device", "--config", "c2",
+                 "--shares", model, "--steps", 3, "--warmup", 3, "--e2e-steps", 1,
+                 "--no-cpu-baseline")
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["config"]["shares"] == [128, 128]
