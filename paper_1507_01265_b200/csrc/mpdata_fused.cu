@@ -737,10 +737,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const int r = wrow + rr;
             if (r < C::HALO || r >= RR - C::HALO || j0 + r - C::HALO >= m) continue;
             const int g = gj[rr] + k0;
-            vstore(dstb + dplane * a.plane + g, vload<T, K>(a.out + pl(t) + g));
+            // L2-coherent load: a.out was written by this kernel
+            vstore(dstb + dplane * a.plane + g, vload_cg<T, K>(a.out + pl(t) + g));
           }
         }
       }
+      // The pushes may target a peer GPU (NVLink): make them visible system-wide
+      // before this kernel completes and the neighbour's flag word is raised.
+      if (tl < th || ul < uh) __threadfence_system();
     }
   }
 #undef KMG

@@ -43,6 +43,29 @@ __device__ __forceinline__ Vec<T, K> vload(const T* p) {  // global, read-only p
   return r;
 }
 
+// Global load through L2 only (coherent with this kernel's own earlier stores).
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> vload_cg(const T* p) {
+  Vec<T, K> r;
+  if constexpr (sizeof(T) == 8 && K == 4) {
+    const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
+  } else if constexpr (sizeof(T) == 8 && K == 2) {
+    const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+    r.e[0] = a.x; r.e[1] = a.y;
+  } else if constexpr (sizeof(T) == 4 && K == 4) {
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(p));
+    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = a.z; r.e[3] = a.w;
+  } else if constexpr (sizeof(T) == 4 && K == 2) {
+    const float2 a = __ldcg(reinterpret_cast<const float2*>(p));
+    r.e[0] = a.x; r.e[1] = a.y;
+  } else {
+    r.e[0] = __ldcg(p);
+  }
+  return r;
+}
+
 template <class T, int K>
 __device__ __forceinline__ Vec<T, K> sload(const T* p) {  // shared
   Vec<T, K> r;
