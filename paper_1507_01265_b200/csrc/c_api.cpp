@@ -269,9 +269,20 @@ int imb_group_create(const imb_domain* global, const imb_opts* opts, int nteams,
       grp->teams[static_cast<std::size_t>(g)]->set_ring(left, right);
       for (imb::rt::Team* nb : {left, right}) {
         if (nb->device() == devices[g]) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, devices[g], nb->device());
+        if (!can) {  // the kernel cannot store into that device: pull with peer copies
+          grp->teams[static_cast<std::size_t>(g)]->set_push_ok(false);
+          continue;
+        }
         cudaSetDevice(devices[g]);
         const cudaError_t e = cudaDeviceEnablePeerAccess(nb->device(), 0);
-        if (e != cudaSuccess) cudaGetLastError();  // already enabled / unsupported: copies still work
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+        } else if (e != cudaSuccess) {
+          cudaGetLastError();
+          grp->teams[static_cast<std::size_t>(g)]->set_push_ok(false);
+        }
       }
     }
     grp->handles.resize(static_cast<std::size_t>(nteams));
@@ -332,7 +343,7 @@ int imb_group_run(imb_group* g, int steps, double* per_team_s, double* wall_s) {
       cudaEventRecord(t0[q], g->teams[q]->stream());
     }
     bool flags = g->sync == IMB_GROUP_SYNC_FLAGS;
-    for (auto& t : g->teams) flags = flags && t->fused();
+    for (auto& t : g->teams) flags = flags && t->fused() && t->push_ok();
     for (int s = 0; s < steps; ++s) {
       bool ready = flags;
       for (auto& t : g->teams) ready = ready && t->halos_ready();

@@ -905,9 +905,9 @@ void Team::group_compute() {
   if (tmp_[0] == nullptr) {
     // push targets: the neighbours' output buffers of this step (their
     // pointers are swapped only in group_finish, after every launch)
-    push_lo_ = left_->xn_;
+    push_lo_ = push_ok_ ? left_->xn_ : nullptr;
     push_lo_ni_ = left_->ni_;
-    push_hi_ = right_->xn_;
+    push_hi_ = push_ok_ ? right_->xn_ : nullptr;
     swap_after_ = false;
     compute_step();
     swap_after_ = true;
@@ -963,7 +963,7 @@ void* Team::out_buffer(std::uint64_t s) const {
 void Team::group_finish(bool signal) {
   if (tmp_[0] == nullptr) {
     std::swap(x_, xn_);
-    halo_fresh_ = true;
+    halo_fresh_ = push_ok_ && left_->push_ok_ && right_->push_ok_;
   }
   if (signal) {  // keep the flag protocol's counters in step (flag mode after an event step)
     MemOps& ops = memops();

@@ -72,6 +72,11 @@ class Team {
     left_ = left;
     right_ = right;
   }
+  // False when this team's device cannot store into a neighbour's device
+  // memory (no peer access): its kernel then pushes nothing and the ring
+  // falls back to pulling the edge planes with peer copies every step.
+  void set_push_ok(bool ok) { push_ok_ = ok; }
+  bool push_ok() const { return push_ok_; }
 
   // Group stepping, issued by imb_group in four host phases per step, each
   // over all teams before the next: (1) record "x of this step is complete";
@@ -147,6 +152,7 @@ class Team {
   std::int64_t push_lo_ni_ = 0;
   bool halo_fresh_ = false;
   bool swap_after_ = true;
+  bool push_ok_ = true;
   std::uint64_t* flags_ = nullptr;  // [0]/[1] left/right neighbour's finished steps,
                                     // [2]/[3] their host-rewrite epochs (IPC ring)
   struct IpcPeer {
