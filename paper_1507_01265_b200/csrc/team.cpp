@@ -172,6 +172,15 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
   if (device < 0 || device >= count)
     throw ConfigError("device " + std::to_string(device) + " not present (" +
                       std::to_string(count) + " visible)");
+  try {
+    acquire();
+  } catch (...) {
+    release();  // the destructor does not run for a throwing constructor
+    throw;
+  }
+}
+
+void Team::acquire() {
   IMB_CUDA(cudaSetDevice(device_));
   IMB_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_));
   IMB_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
@@ -203,7 +212,9 @@ Team::Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, i
   IMB_CUDA(cudaStreamSynchronize(cs_));
 }
 
-Team::~Team() {
+Team::~Team() { release(); }
+
+void Team::release() noexcept {
   cudaSetDevice(device_);
   if (cs_) cudaStreamSynchronize(cs_);
   if (xs_) cudaStreamSynchronize(xs_);

@@ -153,6 +153,8 @@ class Team {
   bool halo_fresh_ = false;
   bool swap_after_ = true;
   bool push_ok_ = true;
+  void acquire();           // device resources (streams, events, pool); throws
+  void release() noexcept;  // frees whatever acquire() obtained
   std::uint64_t* flags_ = nullptr;  // [0]/[1] left/right neighbour's finished steps,
                                     // [2]/[3] their host-rewrite epochs (IPC ring)
   struct IpcPeer {
