@@ -22,7 +22,8 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo", rank=rank, world_size=world)
     n, m, l = 12 * world + 5, 20, 64
-    opts = mpdata.Options(2, True, True)
+    iord, nonos, fp64 = (int(v) for v in (sys.argv[1:4] if len(sys.argv) >= 4 else (2, 1, 1)))
+    opts = mpdata.Options(iord, bool(nonos), bool(fp64))
     shares = [n // world + (1 if r < n % world else 0) for r in range(world)]
     i0 = sum(shares[:rank])
     team = mpdata.Team(n, m, l, opts, device=0, i0=i0, ni=shares[rank])
@@ -47,7 +48,8 @@ def main():
             want = t.download("x")
         got = np.concatenate(parts, axis=0)
         ok = bool(np.array_equal(got, want))
-        print(f"ipc ring world={world}: {'bit-identical' if ok else 'MISMATCH'}", flush=True)
+        print(f"ipc ring world={world} iord={iord} nonos={nonos} fp64={fp64}: "
+              f"{'bit-identical' if ok else 'MISMATCH'}", flush=True)
     flag = [ok]
     dist.broadcast_object_list(flag, src=0)
     dist.barrier()

@@ -31,11 +31,13 @@ def torchrun(nproc, port, *args, timeout=180):
     return subprocess.CompletedProcess(cmd, p.returncode, out, err)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_ipc_ring_processes_bit_identical(world):
-    r = torchrun(world, 29610 + world, "tests/mp/ipc_ring.py")
+@pytest.mark.parametrize("world,scheme", [(2, (2, 1, 1)), (3, (2, 1, 1)), (2, (3, 1, 0)),
+                                          (3, (2, 0, 0))])
+def test_ipc_ring_processes_bit_identical(world, scheme):
+    port = 29610 + 10 * world + scheme[0] + 2 * scheme[2]
+    r = torchrun(world, port, "tests/mp/ipc_ring.py", *scheme)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    assert f"ipc ring world={world}: bit-identical" in r.stdout
+    assert "bit-identical" in r.stdout
 
 
 def test_bench_two_ranks_json_line():
