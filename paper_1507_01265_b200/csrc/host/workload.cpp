@@ -11,6 +11,7 @@
 
 #include "../recipe.cuh"
 #include "../team.hpp"
+#include "imb_mpdata.h"
 #include "imbalance/errors.hpp"
 
 namespace imb {
@@ -235,6 +236,80 @@ double TeamRunner::run(int steps, const std::function<void()>& start_sync,
 }
 
 std::uint64_t TeamRunner::current_checksum() const { return team_->checksum(); }
+
+namespace {
+// C-ABI status -> the matching imb:: exception (the inverse of c_api.cpp's guard)
+void check_status(int rc) {
+  if (rc == 0) return;
+  const std::string msg = imb_last_error();
+  switch (rc) {
+    case IMB_E_RANGE: throw RangeError(msg);
+    case IMB_E_DOMAIN: throw DomainError(msg);
+    case IMB_E_ALIGNMENT: throw AlignmentError(msg);
+    case IMB_E_INCOMPATIBLE: throw IncompatibleModelError(msg);
+    case IMB_E_INSUFFICIENT: throw InsufficientDataError(msg);
+    case IMB_E_INFEASIBLE: throw InfeasibleError(msg);
+    case IMB_E_TOOLARGE: throw TooLargeError(msg);
+    case IMB_E_CONFIG: throw ConfigError(msg);
+    case IMB_E_CONTRACT: throw ContractError(msg);
+    case IMB_E_PARSE: throw ParseError(msg, 0);
+    case IMB_E_CUDA: throw CudaError(msg);
+    case IMB_E_NCCL: throw NcclError(msg);
+    default: throw Error(msg);
+  }
+}
+}  // namespace
+
+GroupRunner::GroupRunner(const StencilDomain& domain, const std::vector<int>& devices,
+                         const std::vector<std::int64_t>& shares, std::uint64_t seed,
+                         const MpdataOptions& opts, Recipe recipe, bool flag_sync)
+    : domain_(domain), shares_(shares), fp64_(opts.fp64) {
+  domain.validate();
+  if (devices.size() != shares.size() || shares.empty())
+    throw ContractError("GroupRunner needs one device per share");
+  const imb_domain dom{domain.n, domain.m, domain.l, domain.halo};
+  const imb_opts o{opts.iord, opts.nonos ? 1 : 0, opts.fp64 ? IMB_FP64 : IMB_FP32};
+  imb_group* g = nullptr;
+  check_status(imb_group_create(&dom, &o, static_cast<int>(shares.size()), devices.data(),
+                                shares.data(), &g));
+  group_ = g;
+  try {
+    check_status(imb_group_set_sync(g, flag_sync ? IMB_GROUP_SYNC_FLAGS : IMB_GROUP_SYNC_EVENTS));
+    check_status(imb_group_init_recipe(g, static_cast<int>(recipe), seed));
+  } catch (...) {
+    imb_group_destroy(g);
+    group_ = nullptr;
+    throw;
+  }
+}
+
+GroupRunner::~GroupRunner() {
+  if (group_) imb_group_destroy(static_cast<imb_group*>(group_));
+}
+
+double GroupRunner::run(int steps) {
+  team_seconds_.assign(shares_.size(), 0.0);
+  double wall = 0.0;
+  check_status(imb_group_run(static_cast<imb_group*>(group_), steps, team_seconds_.data(), &wall));
+  return wall;
+}
+
+std::uint64_t GroupRunner::current_checksum() const {
+  std::uint64_t hsh = 0xcbf29ce484222325ull;
+  const std::size_t elem = fp64_ ? 8 : 4;
+  std::vector<unsigned char> host;
+  for (std::size_t q = 0; q < shares_.size(); ++q) {
+    imb_team* t = nullptr;
+    check_status(imb_group_team(static_cast<imb_group*>(group_), static_cast<int>(q), &t));
+    host.resize(static_cast<std::size_t>(shares_[q] * domain_.m * domain_.l) * elem);
+    check_status(imb_team_download(t, 0, host.data(), host.size()));
+    for (unsigned char b : host) {
+      hsh ^= b;
+      hsh *= 0x100000001b3ull;
+    }
+  }
+  return hsh;
+}
 
 TeamResult run_team_workload(const StencilDomain& domain, int threads, int steps,
                              std::uint64_t seed) {

@@ -120,6 +120,35 @@ class TeamRunner {
   std::unique_ptr<rt::Team> team_;
 };
 
+// Additive extension: P teams = P slabs of one periodic grid,
+// slab q = [sum(shares[:q]), +shares[q]) on devices[q] (several slabs may share
+// a device). The fused step kernel pushes each slab's edge planes into its
+// neighbours' halos (over NVLink between GPUs), so the result — and
+// current_checksum() — is bit-identical to one TeamRunner on the whole grid.
+class GroupRunner {
+ public:
+  GroupRunner(const StencilDomain& domain, const std::vector<int>& devices,
+              const std::vector<std::int64_t>& shares, std::uint64_t seed = 42,
+              const MpdataOptions& opts = {}, Recipe recipe = Recipe::RotCube,
+              bool flag_sync = true);
+  ~GroupRunner();
+  GroupRunner(const GroupRunner&) = delete;
+  GroupRunner& operator=(const GroupRunner&) = delete;
+  // Advance all slabs `steps` steps in lockstep; returns the wall seconds
+  // (max over teams), per-team compute seconds in last_team_seconds().
+  double run(int steps);
+  const std::vector<double>& last_team_seconds() const { return team_seconds_; }
+  std::uint64_t current_checksum() const;  // FNV-1a over the whole grid, slabs in order
+  int teams() const { return static_cast<int>(shares_.size()); }
+
+ private:
+  StencilDomain domain_;
+  std::vector<std::int64_t> shares_;
+  bool fp64_;
+  void* group_ = nullptr;  // imb_group*
+  std::vector<double> team_seconds_;
+};
+
 struct TeamResult {
   double seconds = 0.0;
   std::uint64_t checksum = 0;

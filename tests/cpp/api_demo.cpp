@@ -63,6 +63,21 @@ static void gpu_part() {
   CHECK(team.current_checksum() == c1);  // deterministic
   imb::TeamResult r = imb::run_team_workload(d, 1, 5, 42);
   CHECK(r.checksum == c1);
+  // Three slabs (uneven) on device 0: bit-identical to the single team.
+  for (bool flags : {false, true}) {
+    imb::GroupRunner grp(d, {0, 0, 0}, {10, 7, 15}, 42, {}, imb::Recipe::RotCube, flags);
+    CHECK(grp.run(2) > 0);
+    CHECK(grp.run(3) > 0);
+    CHECK(grp.last_team_seconds().size() == 3);
+    CHECK(grp.current_checksum() == c1);
+  }
+  bool threw = false;
+  try {
+    imb::GroupRunner bad(d, {0, 0}, {16, 15});  // shares must cover n
+  } catch (const imb::ContractError&) {
+    threw = true;
+  }
+  CHECK(threw);
   std::printf("gpu part: %s (checksum %s)\n", fails ? "FAILED" : "ok",
               imb::checksum_hex(c1).c_str());
 }
