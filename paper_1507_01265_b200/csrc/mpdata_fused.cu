@@ -114,6 +114,7 @@ struct Args {
   // one bulk L2 prefetch per input field for the plane `pf` planes beyond
   // the newest one the donor stage reads, so its first touch is an L2 hit.
   int pf;
+  int push_sys;  // push targets may be on a peer GPU (system-scope fence)
 };
 
 // MODE 0: one IORD=2 step. MODE 1: donor + first corrective pass of an
@@ -742,9 +743,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
         }
       }
-      // The pushes may target a peer GPU (NVLink): make them visible system-wide
-      // before this kernel completes and the neighbour's flag word is raised.
-      if (tl < th || ul < uh) __threadfence_system();
+      // Pushes into a peer GPU (NVLink) are made visible system-wide before
+      // this kernel completes and the neighbour's flag word is raised.
+      if (a.push_sys && (tl < th || ul < uh)) __threadfence_system();
     }
   }
 #undef KMG
@@ -907,6 +908,7 @@ int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T*
   if (iord != 2) return 0;
   Args<T> a{x, u, v, w, h, out, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
             push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
+  a.push_sys = push.sys ? 1 : 0;
   return nonos ? dispatch_l<T, true, 0>(fs, a, num_sms, st)
                : dispatch_l<T, false, 0>(fs, a, num_sms, st);
 }
@@ -925,6 +927,7 @@ int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, cons
   int n = dispatch_l<T, true, 1>(f1, a1, num_sms, st);
   Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr,
              push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
+  a2.push_sys = push.sys ? 1 : 0;
   n += dispatch_l<T, true, 2>(fs, a2, num_sms, st);
   return n;
 }

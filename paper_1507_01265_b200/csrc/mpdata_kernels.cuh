@@ -55,6 +55,7 @@ struct HaloPush {
   T* lo = nullptr;          // left neighbour's output buffer
   std::int64_t lo_ni = 0;   // left neighbour's interior planes
   T* hi = nullptr;          // right neighbour's output buffer
+  bool sys = false;         // a target is on another GPU: fence system-wide after the stores
 };
 // Segmentation of a streaming launch: per j-tile of `tj` rows, kseg
 // segments of lseg planes plus one remainder segment (blocks issued longest

@@ -390,7 +390,8 @@ void Team::compute_step_t() {
   T* out = static_cast<T*>(xn_);
   if (tmp_[0] == nullptr) {
     dev::FusedShape fs{m_, l_, ni_, R_, 0, ni_};
-    dev::HaloPush<T> push{static_cast<T*>(push_lo_), push_lo_ni_, static_cast<T*>(push_hi_)};
+    dev::HaloPush<T> push{static_cast<T*>(push_lo_), push_lo_ni_, static_cast<T*>(push_hi_),
+                          push_sys_};
     if (opt_.iord == 3)
       launches_ += dev::launch_fused3<T>(
           fs, x, u, v, w, h, static_cast<T*>(ext_[0]), static_cast<T*>(ext_[1]),
@@ -401,6 +402,7 @@ void Team::compute_step_t() {
                                         cs_, push);
     IMB_CUDA(cudaGetLastError());
     push_lo_ = push_hi_ = nullptr;
+    push_sys_ = false;
     if (swap_after_) std::swap(x_, xn_);
     return;
   }
@@ -798,6 +800,7 @@ void Team::connect_ipc(const unsigned char* left_blob, const unsigned char* righ
     p.off_xn = b.off_xn;
     p.ni = b.ni;
     p.step0 = b.step0;
+    p.device = b.device;
     for (int f = 0; f < 4; ++f) p.off_st[f] = b.off_st[f];
     p.opened = true;
   };
@@ -877,6 +880,7 @@ void Team::ipc_step() {
   push_lo_ = ipc_left_.buffer(static_cast<std::int64_t>(s));
   push_lo_ni_ = ipc_left_.ni;
   push_hi_ = ipc_right_.buffer(static_cast<std::int64_t>(s));
+  push_sys_ = ipc_left_.device != device_ || ipc_right_.device != device_;
   swap_after_ = false;
   compute_step();
   swap_after_ = true;
@@ -919,6 +923,7 @@ void Team::group_compute() {
     push_lo_ = push_ok_ ? left_->xn_ : nullptr;
     push_lo_ni_ = left_->ni_;
     push_hi_ = push_ok_ ? right_->xn_ : nullptr;
+    push_sys_ = left_->device_ != device_ || right_->device_ != device_;
     swap_after_ = false;
     compute_step();
     swap_after_ = true;
@@ -952,6 +957,7 @@ void Team::group_flag_step() {
   push_lo_ = left_->out_buffer(s);
   push_lo_ni_ = left_->ni_;
   push_hi_ = right_->out_buffer(s);
+  push_sys_ = left_->device_ != device_ || right_->device_ != device_;
   swap_after_ = false;
   compute_step();
   swap_after_ = true;

@@ -153,6 +153,7 @@ class Team {
   bool halo_fresh_ = false;
   bool swap_after_ = true;
   bool push_ok_ = true;
+  bool push_sys_ = false;  // the current push targets include a peer GPU
   void acquire();           // device resources (streams, events, pool); throws
   void release() noexcept;  // frees whatever acquire() obtained
   std::uint64_t* flags_ = nullptr;  // [0]/[1] left/right neighbour's finished steps,
@@ -161,6 +162,7 @@ class Team {
     char* pool = nullptr;            // mapped neighbour pool (or this team's own)
     std::uint64_t* flags = nullptr;  // mapped neighbour flag words
     std::int64_t off_x = 0, off_xn = 0, ni = 0, step0 = 0;
+    int device = -1;
     std::int64_t off_st[4] = {0, 0, 0, 0};
     bool opened = false;             // this process opened (and must close) it
     void* buffer(std::int64_t s) const {  // the buffer that peer writes in step s
