@@ -32,7 +32,8 @@ def main():
     dist.all_gather_object(blobs, team.ipc_export())
     team.connect_ipc(blobs[(rank - 1) % world], blobs[(rank + 1) % world], world, rank)
     dist.barrier()
-    team.run(3)
+    extra = int(os.environ.get("IPC_RING_STEPS", "0"))  # stress runs: more steps per call
+    team.run(3 + extra)
     team.run(2)  # continues across calls
     # host-buffer step through the same ring (rewrite epochs)
     x = team.download("x")
@@ -44,7 +45,7 @@ def main():
     if rank == 0:
         with mpdata.Team(n, m, l, opts, device=0) as t:
             t.init_recipe(2, 11)
-            t.run(6)
+            t.run(6 + extra)
             want = t.download("x")
         got = np.concatenate(parts, axis=0)
         ok = bool(np.array_equal(got, want))
