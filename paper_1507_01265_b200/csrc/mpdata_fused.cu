@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <functional>
@@ -806,14 +807,24 @@ template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MO
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
   using C = Cfg<T, L, RW, NW, NS, NONOS, WPR>;
   auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, WPR>;
-  static bool configured = false;
+  // Function attributes are per device: configure each device once (a group
+  // or a measurement may drive several GPUs from one process and thread pool).
+  static std::atomic<std::uint64_t> configured{0};
+  static std::mutex mu;
   static int per_sm = 1;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, C::SMEM);
-    if (per_sm < 1) per_sm = 1;
-    configured = true;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!(configured.load(std::memory_order_relaxed) & bit)) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(C::SMEM));
+      int n = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::NT, C::SMEM);
+      per_sm = n < 1 ? 1 : n;
+      configured.fetch_or(bit, std::memory_order_release);
+    }
   }
   static const int warm_env = [] {
     const char* e = std::getenv("IMB_WARM");  // experiment: warm-up cost in plane-times
