@@ -114,18 +114,25 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, steps, threads):
-    """Times the CPU restatement (oracle/) on a slab sample of the workload grid."""
+def cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, steps, threads, budget_s=0.0):
+    """Times the CPU restatement (oracle/) on a slab sample of the workload grid.
+
+    With ``budget_s`` > 0 the step count is raised until the timed region
+    covers about that many seconds (a bounded sample of the workload)."""
     import numpy as np
 
     from oracle import oracle as O
     dt = np.float64 if fp64 else np.float32
     f = O.init_fields(recipe, n, m, l, seed=42, i0=0, ni=planes, dtype=dt)
+    t0 = time.perf_counter()
     O.run(*f, iord=iord, nonos=nonos, steps=1, threads=threads)  # warm-up / first touch
+    one = time.perf_counter() - t0
+    if budget_s > 0:
+        steps = max(steps, min(1000, int(budget_s / max(one, 1e-6))))
     t0 = time.perf_counter()
     O.run(*f, iord=iord, nonos=nonos, steps=steps, threads=threads)
     dt_s = time.perf_counter() - t0
-    return planes * m * l * steps / dt_s / 1e9, dt_s
+    return planes * m * l * steps / dt_s / 1e9, dt_s, steps
 
 
 def run_reference(args, cfg):
@@ -134,12 +141,12 @@ def run_reference(args, cfg):
         return
     n, m, l, iord, nonos, fp64, recipe, desc = cfg
     threads = os.cpu_count() or 1
-    planes = min(n, 64)
+    planes = min(n, 128)
     vals = []
     for _ in range(max(args.warmup, 0)):
         cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, 1, threads)
     for _ in range(args.steps):
-        v, _ = cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, 1, threads)
+        v, _, _ = cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, 1, threads)
         vals.append(v)
     value = statistics.median(vals)
     sample = f"{planes}x{m}x{l} periodic slab of the {n}x{m}x{l} grid, 1 step per sample"
@@ -327,10 +334,11 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        planes = min(n, 32)
-        v, secs = cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, 2, threads)
+        planes = min(n, 128)
+        v, secs, nst = cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, 2, threads,
+                                       budget_s=10.0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"2 steps on a {planes}x{m}x{l} periodic slab of the "
+                                "sample": f"{nst} steps on a {planes}x{m}x{l} periodic slab of the "
                                           f"{n}x{m}x{l} grid ({secs:.1f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
