@@ -336,7 +336,7 @@ def main():
         threads = os.cpu_count() or 1
         planes = min(n, 128)
         v, secs, nst = cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, 2, threads,
-                                       budget_s=10.0)
+                                       budget_s=15.0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"{nst} steps on a {planes}x{m}x{l} periodic slab of the "
                                           f"{n}x{m}x{l} grid ({secs:.1f} s)"}

@@ -21,6 +21,9 @@ KEYS = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wf"),
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "gld_sectors"),
     ("l1tex__t_sector_hit_rate.pct", "l1hit%"),
+    ("lts__t_sector_hit_rate.pct", "l2hit%"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "l2rd_sectors"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "l2_to_l1_bytes"),
     ("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "dfma"),
     ("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", "dmul"),
     ("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "dadd"),
