@@ -25,5 +25,7 @@ with mpdata.Team(n, m, l, opts) as t:
     t.run(a.warm)
     t0 = time.perf_counter()
     comp, wall = t.run(a.steps)
+    if a.fp32:
+        desc = desc.replace("fp64", "fp32")
     print(f"{desc}: {a.steps} steps compute {comp*1e3:.3f} ms wall {wall*1e3:.3f} ms "
           f"-> {n*m*l*a.steps/wall/1e9:.2f} Gcell/s, launches {t.launches}")
