@@ -149,6 +149,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   const int j0 = tile * C::TJ;
   const int m = a.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef IMB_CHECK_SELFTEST  // proves a failing assert traps (tools/checked_build.sh --selftest)
+  IMB_ASSERT(blockIdx.x != 0 || threadIdx.x != 0, "selftest", 0);
+#endif
   const int wrow = (warp / WPR) * RW;        // first region row of this warp
   const int wcol = (warp % WPR) * (L / WPR);  // first k of this warp's row part
 
@@ -161,10 +164,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     j = ((j % m) + m) % m;
     gj[rr] = j * L;
     gjm[rr] = (j == 0 ? m - 1 : j - 1) * L;
+    IMB_ASSERT(j >= 0 && j < m, "row outside the plane", j);
     gjp[rr] = (j == m - 1 ? 0 : j + 1) * L;
   }
   auto slot3 = [](int p) { return C::NX1 == 4 ? ((p + 8) & 3) : (p + 6) % 3; };  // p >= -3
-  auto pl = [&](int p) { return static_cast<long long>(p + a.R) * a.plane; };
+  auto pl = [&](int p) {
+    IMB_ASSERT(p + a.R >= 0 && p < a.ni + a.R, "plane outside the padded slab", p);
+    return static_cast<long long>(p + a.R) * a.plane;
+  };
   // cell group c = (row rr, segment sg): first k of this lane in the segment
   auto k0of = [&](int c) { return wcol + (c % NS) * 32 * K + lane * K; };
   // MODE 1: plane t+1 values of an own tile row are stored once (segments
@@ -740,6 +747,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             if (r < C::HALO || r >= RR - C::HALO || j0 + r - C::HALO >= m) continue;
             const int g = gj[rr] + k0;
             // L2-coherent load: a.out was written by this kernel
+            IMB_ASSERT(pass == 0 ? (dplane >= a.lo_ni + a.R && dplane < a.lo_ni + 2 * a.R)
+                                 : (dplane >= 0 && dplane < a.R),
+                       "halo push plane", dplane);
             vstore(dstb + dplane * a.plane + g, vload_cg<T, K>(a.out + pl(t) + g));
           }
         }

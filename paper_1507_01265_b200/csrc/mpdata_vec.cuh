@@ -6,10 +6,37 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 namespace imb::dev {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Checked build (-DIMB_CHECKED, tools/checked_build.sh): device-side bounds
+// asserts on plane indices, rows and shared-memory offsets — the stand-in for
+// compute-sanitizer, which this GPU pool does not allow.
+#ifdef IMB_CHECKED
+#define IMB_ASSERT(cond, what, v)                                                          \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("IMB_CHECKED %s: %lld (block %d thread %d)\n", what, static_cast<long long>(v), \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                  \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+__device__ __forceinline__ void check_shared(const void* p, unsigned bytes) {
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  extern __shared__ unsigned char imb_smem_base[];
+  const long long off = static_cast<long long>(__cvta_generic_to_shared(p)) -
+                        static_cast<long long>(__cvta_generic_to_shared(imb_smem_base));
+  IMB_ASSERT(__isShared(p) && off >= 0 && off + bytes <= dyn, "shared offset", off);
+}
+#else
+#define IMB_ASSERT(cond, what, v) ((void)0)
+__device__ __forceinline__ void check_shared(const void*, unsigned) {}
+#endif
 
 __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes));
@@ -68,6 +95,7 @@ __device__ __forceinline__ Vec<T, K> vload_cg(const T* p) {
 
 template <class T, int K>
 __device__ __forceinline__ Vec<T, K> sload(const T* p) {  // shared
+  check_shared(p, sizeof(T) * K);
   Vec<T, K> r;
   if constexpr (sizeof(T) == 8 && K == 4) {
     const double2 a = reinterpret_cast<const double2*>(p)[0];
@@ -90,6 +118,9 @@ __device__ __forceinline__ Vec<T, K> sload(const T* p) {  // shared
 
 template <class T, int K>
 __device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or global
+#ifdef IMB_CHECKED
+  if (__isShared(p)) check_shared(p, sizeof(T) * K);
+#endif
   if constexpr (sizeof(T) == 8 && K == 4) {
     reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
     reinterpret_cast<double2*>(p)[1] = make_double2(v.e[2], v.e[3]);
