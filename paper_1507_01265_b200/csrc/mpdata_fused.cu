@@ -188,13 +188,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // neighbour helpers: G = global source row, S = shared source row
 #define KMG(vec, row, k0) kminus<L, NS * WPR, true>(vec, row, k0, lane)
 #define KPG(vec, row, k0) kplus<L, NS * WPR, true>(vec, row, k0, lane)
-#ifndef IMB_SMEM_RELOAD  // shuffles measured faster than k+-1 smem reloads (C2 -7%)
-#define KMS(vec, row, k0) kminus<L, NS * WPR, false>(vec, row, k0, lane)
-#define KPS(vec, row, k0) kplus<L, NS * WPR, false>(vec, row, k0, lane)
+  // k+-1 of a shared-memory row: fp64 shuffles (smem reloads measured -3 % C4,
+  // -6 % C2), fp32 re-reads the one out-of-vector value from the row (+1.4 % C4,
+  // +1 % C2 over shuffles).
+#ifndef IMB_SMEM_RELOAD
+  constexpr bool SRL = sizeof(T) == 4;
 #else
-#define KMS(vec, row, k0) kminus_s<L>(vec, row, k0)
-#define KPS(vec, row, k0) kplus_s<L>(vec, row, k0)
+  constexpr bool SRL = true;
 #endif
+#define KMS(vec, row, k0) \
+  (SRL ? kminus_s<L>(vec, row, k0) : kminus<L, NS * WPR, false>(vec, row, k0, lane))
+#define KPS(vec, row, k0) \
+  (SRL ? kplus_s<L>(vec, row, k0) : kplus<L, NS * WPR, false>(vec, row, k0, lane))
 
   // psi^n star extrema (STARC): of plane t+1 (nmx), t+2 (nmx_mid, EARLY) and
   // the donor's newest plane (nmx_new)
