@@ -8,7 +8,7 @@ implementation in csrc/host/, so Python adds no arithmetic of its own.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Iterable, Optional, Sequence
 
 from . import _lib

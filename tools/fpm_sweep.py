@@ -18,7 +18,6 @@
 """
 import argparse
 import json
-import statistics
 import sys
 from pathlib import Path
 
