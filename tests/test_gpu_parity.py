@@ -318,3 +318,32 @@ def test_group_decomposition_fused_is_bit_identical(shares, opts):
     g.run(4)
     np.testing.assert_array_equal(g.download("x"), single)
     g.close()
+
+
+@pytest.mark.parametrize("shape", [(5, 18, 128), (7, 19, 128), (16, 47, 128), (6, 130, 128)])
+@pytest.mark.parametrize("iord", [2, 3])
+def test_fp32_staged_inputs_parity(orc, shape, iord):
+    # fp32 at l = 128 stages psi^n and h in shared memory with bulk async copies
+    # (rings refilled one iteration ahead): m = 18 is the smallest staged tile
+    # (rows -1..16 without repeats), short slabs give one- and two-plane
+    # segments, m = 130 wraps the last tile's rows.
+    opts = Options(iord=iord, nonos=True, fp64=False)
+    f = orc.init_fields(2, *shape, seed=31, dtype=np.float32)
+    got = gpu_run(f, opts, 3)
+    want = oracle_run(orc, f, opts, 3)
+    assert rel_err(got, want) <= TOL[False]
+
+
+@pytest.mark.parametrize("shares", [[3, 4, 5], [8, 8], [3, 3, 3, 3]])
+def test_group_fp32_staged_is_bit_identical(shares):
+    opts = Options(2, True, False)
+    n, m, l = sum(shares), 21, 128
+    with Team(n, m, l, opts) as t:
+        t.init_recipe(2, 5)
+        t.run(3)
+        single = t.download("x")
+    g = Group(n, m, l, shares, opts=opts)
+    g.init_recipe(2, 5)
+    g.run(3)
+    np.testing.assert_array_equal(g.download("x"), single)
+    g.close()
