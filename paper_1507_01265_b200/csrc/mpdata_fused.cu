@@ -17,6 +17,10 @@
 //    2 of the y/z pseudo-velocities and 2 of each beta; same-column
 //    dependencies along i (x-face velocity, x-flux, the psi^n star extrema)
 //    are register carries.
+//  * Inputs come through L1/L2 (warp 0 bulk-prefetches every plane into L2
+//    one plane ahead). fp32 at l = 128 also stages psi^n and h, the two most
+//    re-read fields, in shared-memory rings filled by bulk async copies (TMA
+//    engine, one mbarrier per slot); fp64 has no shared memory left for it.
 //  * Divisions: fp64 folds the four divisions of a pseudo-velocity into one
 //    reciprocal of hb*dA*dB*dC and the two beta divisions into one, with a
 //    MUFU seed + 2 Newton steps; fp32 uses MUFU.RCP. Both stay inside the
