@@ -212,8 +212,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   auto fill_h = [&](int q) {
     stage_rows(s_hs + hslot(q) * C::HROWS * L, a.h, q, jstage, C::HROWS, &mbar[C::NXS + hslot(q)]);
   };
-  auto wait_x = [&](int q) { mbar_wait(&mbar[xslot(q)], static_cast<unsigned>((q - xb) / C::NXS) & 1u); };
-  auto wait_h = [&](int q) { mbar_wait(&mbar[C::NXS + hslot(q)], static_cast<unsigned>((q - hb) / C::NHS) & 1u); };
+  const unsigned mbar_s = smem_u32(mbar);
+  auto wait_x = [&](int q) {
+    mbar_wait_s(mbar_s + 8u * xslot(q), static_cast<unsigned>((q - xb) >> 2) & 1u);
+  };
+  auto wait_h = [&](int q) {
+    mbar_wait_s(mbar_s + 8u * (C::NXS + hslot(q)), static_cast<unsigned>((q - hb) / C::NHS) & 1u);
+  };
   if constexpr (STG) {
     if (threadIdx.x == 0) {
       for (int i = 0; i < C::NXS + C::NHS; ++i) mbar_init(&mbar[i], 1);
@@ -284,8 +289,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     }
     const int nc_donor = MODE == 2 ? 0 : NC;  // (MODE 2 returned above)
     if constexpr (STG) {
-      wait_x(p - 1);
-      wait_x(p);
+      // donors run in plane order: the older two psi^n planes were waited
+      // for by the previous donor (all three by the segment's first)
+      if (p == ib - 2) {  // (STG implies the limiter: lag 2)
+        wait_x(p - 1);
+        wait_x(p);
+      }
       wait_x(p + 1);
       wait_h(p);
     }

@@ -64,6 +64,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_s(unsigned b, unsigned parity) {  // shared address
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
