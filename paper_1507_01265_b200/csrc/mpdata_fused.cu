@@ -64,6 +64,12 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #ifndef IMB_EARLY_STARC
 #define IMB_EARLY_STARC 1
 #endif
+#ifndef IMB_TWO_F32  // two barriers per plane (see Cfg::TWO): fp32 +7.6 % C4, +4 % C5
+#define IMB_TWO_F32 1
+#endif
+#ifndef IMB_TWO_F64  // fp64: -7 % C4 (224 KB of shared memory leaves 28 KB of L1; spills)
+#define IMB_TWO_F64 0
+#endif
 
 template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR = 1, bool STG = false>
 struct Cfg {
@@ -82,7 +88,13 @@ struct Cfg {
   // variants keep the donor in its own phase.
   static constexpr bool EARLY = NONOS && IMB_EARLY_DONOR && L == 128;  // l=64: measured -3.5%
   static constexpr int NX1 = EARLY ? 4 : 3;  // psi^(1) slots
-  static constexpr int NSLOT = NONOS ? 8 + NX1 : 5;
+  // TWO: the donor of plane t+3 runs with the bounds (phase 2) and the
+  // barrier between the final update (phase 3) and the next plane's
+  // pseudo-velocities goes away; a third y/z-velocity slot keeps the next
+  // plane's pseudo-velocities off the ones a slower warp's final update reads.
+  static constexpr bool TWO = EARLY && (sizeof(T) == 4 ? IMB_TWO_F32 : IMB_TWO_F64);
+  static constexpr int NVW = NONOS ? (TWO ? 3 : 2) : 1;  // y- and z-velocity slots each
+  static constexpr int NSLOT = NONOS ? NX1 + 2 * NVW + 4 : 5;
   // STG: psi^n and h staged in shared memory by bulk async copies (TMA engine)
   // into rings of 4 (psi^n, rows -1..RR) and 5 (h, rows 0..RR-1) planes, each
   // slot with its own mbarrier.
@@ -144,8 +156,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   T* s_x1 = sm;                          // 3 slots of psi^(1), by plane mod 3
   constexpr bool EARLY = C::EARLY && (!STARC || IMB_EARLY_STARC);
   T* s_v = sm + C::NX1 * PL;             // y-face pseudo-velocities
-  T* s_w = s_v + (NONOS ? 2 : 1) * PL;   // z-face pseudo-velocities
-  T* s_bu = s_w + (NONOS ? 2 : 1) * PL;  // beta up,   2 slots (NONOS)
+  T* s_w = s_v + C::NVW * PL;            // z-face pseudo-velocities
+  T* s_bu = s_w + C::NVW * PL;           // beta up,   2 slots (NONOS)
+  constexpr bool TWO = C::TWO;
+  auto vws = [](int p) { return C::NVW == 3 ? (p + 6) % 3 : (p & 1); };  // p >= -3
   T* s_bd = s_bu + 2 * PL;               // beta down, 2 slots (NONOS)
   T* s_xs = s_x1 + C::NSLOT * PL;                 // STG: psi^n ring
   T* s_hs = s_xs + C::NXS * C::XROWS * L;         // STG: h ring
@@ -556,7 +570,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       // mbarrier (a fence.proxy.async here measured -1.5 %).
       if (threadIdx.x == 0) {
         if (t + 5 <= ie + 2) fill_x(t + 5);
-        if (t + 4 <= ie + 1) fill_h(t + 4);
+        if (!TWO && t + 4 <= ie + 1) fill_h(t + 4);
       }
     }
     if (a.pf > 0 && warp == 0 && lane < 5 && !(STG && (lane == 0 || lane == 4))) {
@@ -582,10 +596,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     IMB_ACC(1, 1, 2)
     if constexpr (NONOS) {
       const int p1 = t + 1;
-      T* vA = s_v + (p1 & 1) * PL;              // y-face velocities, plane t+1
-      T* wA = s_w + (p1 & 1) * PL;
-      const T* vB = s_v + ((p1 + 1) & 1) * PL;  // limited, plane t
-      const T* wB = s_w + ((p1 + 1) & 1) * PL;
+      T* vA = s_v + vws(p1) * PL;              // y-face velocities, plane t+1
+      T* wA = s_w + vws(p1) * PL;
+      const T* vB = s_v + vws(t) * PL;         // limited, plane t
+      const T* wB = s_w + vws(t) * PL;
       T* buA = s_bu + (p1 & 1) * PL;            // beta, plane t+1
       T* bdA = s_bd + (p1 & 1) * PL;
       const T* buB = s_bu + ((p1 + 1) & 1) * PL;  // beta, plane t
@@ -593,6 +607,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       stage_pseudo(p1, false, ufresh, vA, wA);
       IMB_T(3)
       nb_sync();
+      if constexpr (STG && TWO) {  // h(t-1)'s last reader, final(t-1), is behind this barrier
+        if (threadIdx.x == 0 && t + 4 <= ie + 1) fill_h(t + 4);
+      }
       IMB_T(4)
       IMB_ACC(2, 2, 3)
       IMB_ACC(3, 3, 4)
@@ -685,6 +702,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
         }
       }
+      if constexpr (TWO) {
+        if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
+      }
       IMB_T(5)
       nb_sync();
       IMB_T(6)
@@ -765,7 +785,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       IMB_T(9)
-      if constexpr (EARLY) {
+      if constexpr (EARLY && !TWO) {
         if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
       }
 #pragma unroll
@@ -782,7 +802,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       IMB_T(7)
-      nb_sync();
+      if constexpr (!TWO) nb_sync();
       IMB_T(8)
       IMB_ACC(6, 6, 9)
       IMB_ACC(8, 9, 7)
