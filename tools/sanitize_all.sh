@@ -1,6 +1,9 @@
 #!/bin/bash
 # compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_cases.py
 # (SURVEY.md §4 item 5). One line per (tool, case): exit code and the summary.
+# Note: the round-1 GPU pool refuses compute-sanitizer (it has left GPUs needing a
+# reset there); tools/checked_build.sh + tests/test_checked.py stand in for it.
+# Kept for machines where the sanitizer is allowed.
 mkdir -p gpurun_out
 CS=${CS:-/usr/local/cuda/bin/compute-sanitizer}
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
