@@ -107,6 +107,20 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: relaunch as N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1 and return its code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "bench.py"), *sys.argv[1:]]
+    print(f"bench: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -136,6 +150,10 @@ def cpu_port_gcells(n, m, l, iord, nonos, fp64, recipe, planes, steps, threads, 
 
 
 def run_reference(args, cfg):
+    """The reference arm: the CPU restatement of the path (oracle/, the
+    reference ships no runnable MPDATA) on the FULL workload grid with every
+    host thread: W untimed steps, then K timed steps in one call (its scratch
+    is allocated once per call, as a resident CPU code would)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
@@ -144,29 +162,22 @@ def run_reference(args, cfg):
     from oracle import oracle as O
     n, m, l, iord, nonos, fp64, recipe, desc = cfg
     threads = os.cpu_count() or 1
-    planes = min(n, 128)
-    f = O.init_fields(recipe, n, m, l, seed=42, i0=0, ni=planes,
-                      dtype=np.float64 if fp64 else np.float32)
+    f = O.init_fields(recipe, n, m, l, seed=42, dtype=np.float64 if fp64 else np.float32)
+    x = O.run(*f, iord=iord, nonos=nonos, steps=max(args.warmup, 0), threads=threads)
     t0 = time.perf_counter()
-    O.run(*f, iord=iord, nonos=nonos, steps=1, threads=threads)  # first touch
-    per = max(1, int(1.0 / max(time.perf_counter() - t0, 1e-6)))  # ~1 s of steps per sample
-    vals = []
-    for i in range(max(args.warmup, 0) + args.steps):
-        t0 = time.perf_counter()
-        O.run(*f, iord=iord, nonos=nonos, steps=per, threads=threads)
-        dt_s = time.perf_counter() - t0
-        if i >= args.warmup:
-            vals.append(planes * m * l * per / dt_s / 1e9)
-    value = statistics.median(vals)
-    sample = (f"{planes}x{m}x{l} periodic slab of the {n}x{m}x{l} grid, {per} steps (~1 s) per "
-              f"timed step, median of {args.steps}")
+    O.run(x, *f[1:], iord=iord, nonos=nonos, steps=args.steps, threads=threads)
+    dt_s = time.perf_counter() - t0
+    value = n * m * l * args.steps / dt_s / 1e9
+    sample = (f"the full {n}x{m}x{l} grid: {args.warmup} untimed + {args.steps} timed steps "
+              f"({dt_s:.1f} s) on {threads} threads")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": planes * m * l / value / 1e6,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": max(world, args.gpus),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if fp64 else "f32", "data": "synthetic (seeded BASELINE recipe)",
         "config": {"workload": desc, "grid": [n, m, l], "iord": iord, "nonos": nonos,
-                   "parallelism": "cpu threads"},
+                   "boundary": "periodic", "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -201,6 +212,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
 
     import numpy as np
     import torch
@@ -210,6 +223,8 @@ def main():
 
     n, m, l, iord, nonos, fp64, recipe, desc = cfg
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -255,6 +270,17 @@ def main():
         uid = [mpdata.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         team.connect_nccl(uid[0], world, rank)
+    me = {"rank": rank, "device": local, "pci": torch.cuda.get_device_properties(local).pci_bus_id
+          if hasattr(torch.cuda.get_device_properties(local), "pci_bus_id") else None,
+          "slab": [i0, shares[rank]], "halo": halo if world > 1 else "self-push"}
+    ranks = [me]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+        if rank == 0:
+            print(f"bench: {world} ranks, halo path {halo}: " +
+                  ", ".join(f"rank {r['rank']} -> cuda:{r['device']} slab {r['slab']}"
+                            for r in ranks), file=sys.stderr, flush=True)
 
     def barrier():
         torch.cuda.synchronize()
@@ -305,11 +331,28 @@ def main():
     local_cells = shares[rank] * m * l
     per_step = comp_max / args.steps
     traffic = None  # DRAM bytes per launch from the committed ncu capture
+    compute = None  # the secondary (compute) floors, from the same capture
     tfile = ROOT / "profiles" / "traffic.json"
+    rec = None
     if tfile.exists():
         rec = json.loads(tfile.read_text()).get(f"{args.config}/{'f64' if fp64 else 'f32'}")
-        if rec and world == 1:
-            traffic = rec["dram_bytes_per_launch"]
+    if rec and world == 1:
+        traffic = rec["dram_bytes_per_launch"]
+        launches_per_step = max(1, round(launches / args.steps))
+        if "warp_inst_per_step" in rec:
+            # issue floor: every warp instruction of a step issued at 4 per SM
+            # per clock (148 SMs, max SM clock); FP pipe floor: the step's
+            # FP64 (fp32: FMA) pipe busy cycles, i.e. its measured utilisation
+            # times its ncu duration. frac = floor / this run's step time.
+            clk = 1965e6
+            issue_ms = rec["warp_inst_per_step"] / (148 * 4 * clk) * 1e3
+            pipe_ms = rec["fp_pipe_active_pct"] / 100.0 * rec["ncu_ms_per_step"]
+            compute = {"issue_floor_ms": issue_ms, "issue_frac": issue_ms / (per_step * 1e3),
+                       "fp_pipe": rec["fp_pipe"], "fp_pipe_floor_ms": pipe_ms,
+                       "fp_pipe_frac": pipe_ms / (per_step * 1e3),
+                       "warp_inst_per_step": rec["warp_inst_per_step"],
+                       "ipc": rec.get("ipc"), "launches_per_step": launches_per_step,
+                       "source": rec.get("source")}
     achieved = local_cells * bytes_per_cell / per_step / 1e9 if world == 1 else \
         max(shares) * m * l * bytes_per_cell / per_step / 1e9
 
@@ -321,6 +364,7 @@ def main():
         "config": {"workload": desc, "grid": [n, m, l], "iord": iord, "nonos": nonos,
                    "boundary": "periodic", "shares": shares,
                    "parallelism": f"slab{world}" + (f" {halo}-halo" if world > 1 else ""),
+                   "ranks": ranks,
                    "l2": f"inputs larger than L2 (5 fields x {cells * elem >> 20} MiB)",
                    # halo planes each GPU sends per step, per direction
                    "halo_bytes_per_gpu_per_step": (2 * mpdata.step_radius(opts) * m * l * elem
@@ -337,7 +381,8 @@ def main():
                      "kernel": ("k_fused (one launch per step; CUDA events on the team compute "
                                 "stream)" if iord == 2 and l in (32, 64, 128) else
                                 "staged step kernels (per-step compute window)"),
-                     "algorithmic_bytes_per_cell": bytes_per_cell, "peak_source": peak_src},
+                     "algorithmic_bytes_per_cell": bytes_per_cell, "peak_source": peak_src,
+                     "compute": compute},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "compute_ms_per_step": per_step * 1e3,

@@ -95,6 +95,13 @@ imb::StencilDomain dom(const imb_domain* d) {
   return s;
 }
 
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw imb::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
 imb::rt::Team& team_of(imb_team* t) {
   need(t, "team");
   return *t->t;
@@ -334,16 +341,33 @@ int imb_group_run(imb_group* g, int steps, double* per_team_s, double* wall_s) {
     need(g, "group");
     if (steps < 0) throw imb::ContractError("steps must be >= 0");
     const std::size_t nt = g->teams.size();
-    std::vector<cudaEvent_t> t0(nt), t1(nt);
+    std::vector<cudaEvent_t> t0(nt, nullptr), t1(nt, nullptr);
+    struct Events {  // destroyed on every exit path, including a throw
+      std::vector<imb::rt::Team*> teams;
+      std::vector<cudaEvent_t>* evs[2];
+      ~Events() {
+        for (auto* v : evs)
+          for (std::size_t q = 0; q < v->size(); ++q)
+            if ((*v)[q]) {
+              cudaSetDevice(teams[q]->device());
+              cudaEventDestroy((*v)[q]);
+            }
+      }
+    } guard_ev{{}, {&t0, &t1}};
+    for (auto& t : g->teams) guard_ev.teams.push_back(t.get());
     for (std::size_t q = 0; q < nt; ++q) {
-      cudaSetDevice(g->teams[q]->device());
-      cudaEventCreate(&t0[q]);
-      cudaEventCreate(&t1[q]);
+      cuda_ok(cudaSetDevice(g->teams[q]->device()), "cudaSetDevice");
+      cuda_ok(cudaEventCreate(&t0[q]), "cudaEventCreate");
+      cuda_ok(cudaEventCreate(&t1[q]), "cudaEventCreate");
       g->teams[q]->take_compute_seconds();
-      cudaEventRecord(t0[q], g->teams[q]->stream());
+      cuda_ok(cudaEventRecord(t0[q], g->teams[q]->stream()), "cudaEventRecord");
     }
-    bool flags = g->sync == IMB_GROUP_SYNC_FLAGS;
-    for (auto& t : g->teams) flags = flags && t->fused() && t->push_ok();
+    // The flag protocol needs fused slabs that push into each other and the
+    // stream memory operations; when it is usable, event steps keep the flag
+    // words in step too, so imb_group_set_sync may switch modes at any time.
+    bool can_flag = imb::rt::stream_memops_available();
+    for (auto& t : g->teams) can_flag = can_flag && t->fused() && t->push_ok();
+    const bool flags = can_flag && g->sync == IMB_GROUP_SYNC_FLAGS;
     for (int s = 0; s < steps; ++s) {
       bool ready = flags;
       for (auto& t : g->teams) ready = ready && t->halos_ready();
@@ -355,23 +379,20 @@ int imb_group_run(imb_group* g, int steps, double* per_team_s, double* wall_s) {
       for (auto& t : g->teams) t->group_mark_ready();
       for (auto& t : g->teams) t->group_pull();
       for (auto& t : g->teams) t->group_compute();
-      for (auto& t : g->teams) t->group_finish(flags);
+      for (auto& t : g->teams) t->group_finish(can_flag);
     }
     double wall = 0.0;
     for (std::size_t q = 0; q < nt; ++q) {
-      cudaSetDevice(g->teams[q]->device());
-      cudaEventRecord(t1[q], g->teams[q]->stream());
-      cudaEventSynchronize(t1[q]);
+      cuda_ok(cudaSetDevice(g->teams[q]->device()), "cudaSetDevice");
+      cuda_ok(cudaEventRecord(t1[q], g->teams[q]->stream()), "cudaEventRecord");
+      cuda_ok(cudaEventSynchronize(t1[q]), "cudaEventSynchronize");
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, t0[q], t1[q]);
+      cuda_ok(cudaEventElapsedTime(&ms, t0[q], t1[q]), "cudaEventElapsedTime");
       wall = std::max(wall, static_cast<double>(ms) * 1e-3);
       const double c = g->teams[q]->take_compute_seconds();
       if (per_team_s) per_team_s[q] = c;
-      cudaEventDestroy(t0[q]);
-      cudaEventDestroy(t1[q]);
     }
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) throw imb::CudaError(cudaGetErrorString(e));
+    cuda_ok(cudaGetLastError(), "group step");
     if (wall_s) *wall_s = wall;
   });
 }

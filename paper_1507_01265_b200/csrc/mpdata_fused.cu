@@ -944,24 +944,27 @@ template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MO
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
   using C = Cfg<T, L, RW, NW, NS, NONOS, WPR, STG>;
   auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, WPR, STG>;
-  // Function attributes are per device: configure each device once (a group
-  // or a measurement may drive several GPUs from one process and thread pool).
-  static std::atomic<std::uint64_t> configured{0};
+  // Function attributes and occupancy are per device: configure each device
+  // once (a group or a measurement may drive several GPUs from one process).
   static std::mutex mu;
-  static int per_sm = 1;
+  static std::map<int, int> per_sm_of;  // device -> resident blocks per SM
   int dev = 0;
-  cudaGetDevice(&dev);
-  const std::uint64_t bit = 1ull << (dev & 63);
-  if (!(configured.load(std::memory_order_acquire) & bit)) {
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  int per_sm = 0;
+  {
     std::lock_guard<std::mutex> lock(mu);
-    if (!(configured.load(std::memory_order_relaxed) & bit)) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(C::SMEM));
-      int n = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::NT, C::SMEM);
-      per_sm = n < 1 ? 1 : n;
-      configured.fetch_or(bit, std::memory_order_release);
+    auto it = per_sm_of.find(dev);
+    if (it == per_sm_of.end()) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(C::SMEM)) != cudaSuccess)
+        return -1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::NT, C::SMEM) != cudaSuccess ||
+          n < 1)
+        return -1;  // the launch could not be resident: report, do not launch
+      it = per_sm_of.emplace(dev, n).first;
     }
+    per_sm = it->second;
   }
   static const int warm_env = [] {
     const char* e = std::getenv("IMB_WARM");  // experiment: warm-up cost in plane-times
@@ -1082,12 +1085,13 @@ int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, cons
   f1.o1 = fs.o1 + 2;
   Args<T> a1{x, u, v, w, h, x2, 0, 0, 0, 0, 0, 0, 0, 0, mx, mn, u2, v2, w2,
              nullptr, nullptr, 0, static_cast<int>(fs.ni)};
-  int n = dispatch_l<T, true, 1>(f1, a1, num_sms, st);
+  const int n = dispatch_l<T, true, 1>(f1, a1, num_sms, st);
+  if (n <= 0) return n;
   Args<T> a2{x2, u2, v2, w2, h, out, 0, 0, 0, 0, 0, 0, 0, 0, mx, mn, nullptr, nullptr, nullptr,
              push.lo, push.hi, static_cast<int>(push.lo_ni), static_cast<int>(fs.ni)};
   a2.push_sys = push.sys ? 1 : 0;
-  n += dispatch_l<T, true, 2>(fs, a2, num_sms, st);
-  return n;
+  const int n2 = dispatch_l<T, true, 2>(fs, a2, num_sms, st);
+  return n2 < 0 ? n2 : n + n2;
 }
 
 template int launch_fused<double>(const FusedShape&, int, int, const double*, const double*,

@@ -144,6 +144,18 @@ MemOps& memops() {
   if (!ops.wait || !ops.write) throw CudaError("stream memory operations unavailable");
   return ops;
 }
+}  // namespace
+
+bool stream_memops_available() {
+  try {
+    (void)memops();
+    return true;
+  } catch (const CudaError&) {
+    return false;
+  }
+}
+
+namespace {
 void memop_check(CUresult r, const char* what) {
   if (r != CUDA_SUCCESS) throw CudaError(std::string(what) + " failed (CUresult " + std::to_string(r) + ")");
 }
@@ -372,6 +384,16 @@ double Team::take_compute_seconds() {
 }
 
 namespace {
+// Fused launchers return the kernels launched, or < 0 when the kernel could
+// not be configured for this device (shared-memory opt-in / occupancy).
+int fused_launched(int n) {
+  if (n < 0) {
+    const cudaError_t e = cudaGetLastError();
+    throw CudaError(std::string("fused step kernel could not be configured: ") +
+                    cudaGetErrorString(e));
+  }
+  return n;
+}
 struct Rng {
   std::int64_t a, b;
 };
@@ -393,13 +415,13 @@ void Team::compute_step_t() {
     dev::HaloPush<T> push{static_cast<T*>(push_lo_), push_lo_ni_, static_cast<T*>(push_hi_),
                           push_sys_};
     if (opt_.iord == 3)
-      launches_ += dev::launch_fused3<T>(
+      launches_ += fused_launched(dev::launch_fused3<T>(
           fs, x, u, v, w, h, static_cast<T*>(ext_[0]), static_cast<T*>(ext_[1]),
           static_cast<T*>(ext_[2]), static_cast<T*>(ext_[3]), static_cast<T*>(ext_[4]),
-          static_cast<T*>(ext_[5]), out, num_sms_, cs_, push);
+          static_cast<T*>(ext_[5]), out, num_sms_, cs_, push));
     else
-      launches_ += dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h, out, num_sms_,
-                                        cs_, push);
+      launches_ += fused_launched(dev::launch_fused<T>(fs, opt_.iord, opt_.nonos, x, u, v, w, h,
+                                                       out, num_sms_, cs_, push));
     IMB_CUDA(cudaGetLastError());
     push_lo_ = push_hi_ = nullptr;
     push_sys_ = false;
@@ -484,15 +506,15 @@ void Team::fused_range(std::int64_t o0, std::int64_t o1) {
   if (o1 <= o0) return;
   dev::FusedShape fs{m_, l_, ni_, R_, o0, o1};
   if (opt_.fp64)
-    launches_ += dev::launch_fused<double>(
+    launches_ += fused_launched(dev::launch_fused<double>(
         fs, opt_.iord, opt_.nonos, static_cast<const double*>(x_), static_cast<const double*>(st_[0]),
         static_cast<const double*>(st_[1]), static_cast<const double*>(st_[2]),
-        static_cast<const double*>(st_[3]), static_cast<double*>(xn_), num_sms_, cs_);
+        static_cast<const double*>(st_[3]), static_cast<double*>(xn_), num_sms_, cs_));
   else
-    launches_ += dev::launch_fused<float>(
+    launches_ += fused_launched(dev::launch_fused<float>(
         fs, opt_.iord, opt_.nonos, static_cast<const float*>(x_), static_cast<const float*>(st_[0]),
         static_cast<const float*>(st_[1]), static_cast<const float*>(st_[2]),
-        static_cast<const float*>(st_[3]), static_cast<float*>(xn_), num_sms_, cs_);
+        static_cast<const float*>(st_[3]), static_cast<float*>(xn_), num_sms_, cs_));
   IMB_CUDA(cudaGetLastError());
 }
 
@@ -563,7 +585,10 @@ void Team::run(int steps, double* compute_s, double* wall_s) {
   IMB_CUDA(cudaEventCreate(&t0));
   IMB_CUDA(cudaEventCreate(&t1));
   IMB_CUDA(cudaEventRecord(t0, cs_));
-  if (!static_halo_ok_) exchange_static();
+  // IPC ring members pull their neighbours' static halos inside ipc_step()
+  // (after both neighbours posted their uploads); a self/NCCL exchange here
+  // would fill them from the wrong slab and mark them valid.
+  if (!static_halo_ok_ && !ipc_) exchange_static();
   ev_used_ = 0;
   // Hiding the exchange behind the interior costs two extra launches for the
   // 2R boundary planes; each streams R planes plus the warm-up on one block

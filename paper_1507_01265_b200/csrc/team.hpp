@@ -42,6 +42,9 @@ void ring_plan(int rank, int nranks, std::int64_t ni, std::int64_t R, RingOp out
 
 class NcclLink;  // defined in team.cpp
 
+// cuStreamWaitValue64 / cuStreamWriteValue64 resolvable on this driver.
+bool stream_memops_available();
+
 class Team {
  public:
   Team(std::int64_t n, std::int64_t m, std::int64_t l, const Options& opt, int device,
@@ -90,7 +93,9 @@ class Team {
   void group_pull();
   void group_compute();
   // phase 4: swap the ping-pong buffers (fused push path); with `signal`,
-  // also announce the step in the neighbours' flag words
+  // also announce the step in the neighbours' flag words. The group signals
+  // on every event step whenever the flag protocol is usable, so switching
+  // the sync mode at any point finds the flag words in step.
   void group_finish(bool signal = false);
   bool halos_ready() const { return static_halo_ok_ && halo_fresh_; }
   // Alternative group protocol for fused slabs: one call per team per step,

@@ -117,7 +117,19 @@ class Team:
         return comp.value, wall.value
 
     def step_host(self, x_in: np.ndarray, x_out: np.ndarray):
-        check(load().imb_team_step_host(self._h, x_in.ctypes.data, x_out.ctypes.data))
+        """One step from host buffers: x_in -> device -> step -> x_out. Both
+        must be slab-shaped; x_out must be a writeable C-contiguous array of
+        the team precision (the C side copies ni*m*l elements each way)."""
+        a = np.ascontiguousarray(x_in, dtype=self.opts.dtype)
+        if a.shape != self.shape:
+            raise _lib.ContractError(f"step_host input shape {a.shape} != slab {self.shape}")
+        if (not isinstance(x_out, np.ndarray) or x_out.shape != self.shape
+                or x_out.dtype != self.opts.dtype or not x_out.flags.c_contiguous
+                or not x_out.flags.writeable):
+            raise _lib.ContractError(
+                f"step_host output must be a writeable C-contiguous {np.dtype(self.opts.dtype)} "
+                f"array of shape {self.shape}")
+        check(load().imb_team_step_host(self._h, a.ctypes.data, x_out.ctypes.data))
 
     def checksum(self) -> int:
         out = C.c_uint64()

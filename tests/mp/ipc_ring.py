@@ -27,7 +27,16 @@ def main():
     shares = [n // world + (1 if r < n % world else 0) for r in range(world)]
     i0 = sum(shares[:rank])
     team = mpdata.Team(n, m, l, opts, device=0, i0=i0, ni=shares[rank])
-    team.init_recipe(2, 11)
+    upload = os.environ.get("IPC_RING_UPLOAD") == "1"
+    fields = None
+    if upload:
+        # host-uploaded x, u, v, w, h (uniform-random, divergent Courant
+        # numbers): the static halos must then come from the neighbours
+        from oracle import oracle as O
+        fields = O.init_fields(0, n, m, l, seed=13, dtype=opts.dtype)
+        team.upload_all(*(f[i0:i0 + shares[rank]] for f in fields))
+    else:
+        team.init_recipe(2, 11)
     blobs = [None] * world
     dist.all_gather_object(blobs, team.ipc_export())
     team.connect_ipc(blobs[(rank - 1) % world], blobs[(rank + 1) % world], world, rank)
@@ -44,12 +53,15 @@ def main():
     ok = True
     if rank == 0:
         with mpdata.Team(n, m, l, opts, device=0) as t:
-            t.init_recipe(2, 11)
+            if upload:
+                t.upload_all(*fields)
+            else:
+                t.init_recipe(2, 11)
             t.run(6 + extra)
             want = t.download("x")
         got = np.concatenate(parts, axis=0)
         ok = bool(np.array_equal(got, want))
-        print(f"ipc ring world={world} iord={iord} nonos={nonos} fp64={fp64}: "
+        print(f"ipc ring world={world} iord={iord} nonos={nonos} fp64={fp64} upload={upload}: "
               f"{'bit-identical' if ok else 'MISMATCH'}", flush=True)
     flag = [ok]
     dist.broadcast_object_list(flag, src=0)

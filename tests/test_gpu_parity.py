@@ -127,6 +127,50 @@ def test_group_flag_sync_is_bit_identical(shares, opts):
     g.close()
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("shares", [[16, 16], [9, 7, 16]])
+def test_group_sync_mode_switching_is_bit_identical(shares):
+    # events -> flags -> events -> flags must neither deadlock (the
+    # flag words are kept in step by every event step) nor change a bit.
+    opts = Options(2, True, True)
+    n, m, l = sum(shares), 20, 64
+    with Team(n, m, l, opts) as t:
+        t.init_recipe(2, 11)
+        t.run(9)
+        single = t.download("x")
+    g = Group(n, m, l, shares, opts=opts)
+    g.init_recipe(2, 11)
+    g.run(2)  # events
+    g.set_sync("flags")
+    g.run(3)
+    g.set_sync("events")
+    g.run(2)
+    g.set_sync("flags")
+    g.run(2)
+    np.testing.assert_array_equal(g.download("x"), single)
+    g.close()
+
+
+def test_step_host_rejects_bad_buffers():
+    # the C side copies ni*m*l elements each way, so the mirror
+    # must refuse wrong dtypes, shapes and non-contiguous or read-only outputs.
+    with Team(16, 8, 32, Options(2, True, True)) as t:
+        t.init_recipe(2, 1)
+        good = np.zeros(t.shape)
+        with pytest.raises(_lib.ContractError):
+            t.step_host(np.zeros((15, 8, 32)), good)
+        with pytest.raises(_lib.ContractError):
+            t.step_host(good, np.zeros(t.shape, dtype=np.float32))
+        with pytest.raises(_lib.ContractError):
+            t.step_host(good, np.zeros((16, 8, 64))[:, :, ::2])
+        ro = np.zeros(t.shape)
+        ro.flags.writeable = False
+        with pytest.raises(_lib.ContractError):
+            t.step_host(good, ro)
+        out = np.zeros(t.shape)
+        t.step_host(good.astype(np.float32), out)  # inputs are converted
+
+
 def test_group_with_uploaded_fields(orc):
     opts = Options(2, True, True)
     f = orc.init_fields(0, 30, 16, 24, seed=3)
