@@ -46,53 +46,60 @@ double reg_inc_beta(double a, double b, double x) {
   return 1.0 - lead * beta_cf(b, a, 1.0 - x) / b;
 }
 
+// Sum and sum of squared deviations in two passes (no cancellation).
+struct Moments {
+  double mean = 0.0;
+  double ssd = 0.0;
+  std::size_t n = 0;
+};
+
+Moments moments(std::span<const double> xs, bool need_spread) {
+  Moments m;
+  m.n = xs.size();
+  if (m.n == 0) throw InsufficientDataError("no observations");
+  if (need_spread && m.n < 2) throw InsufficientDataError("a spread needs two or more observations");
+  double total = 0.0;
+  for (double v : xs) total += v;
+  m.mean = total / static_cast<double>(m.n);
+  if (need_spread)
+    for (double v : xs) m.ssd += (v - m.mean) * (v - m.mean);
+  return m;
+}
+
+double stddev_of(const Moments& m) { return std::sqrt(m.ssd / static_cast<double>(m.n - 1)); }
+
 }  // namespace
 
-double mean(std::span<const double> xs) {
-  if (xs.empty()) throw InsufficientDataError("mean of an empty sample");
-  double s = 0.0;
-  for (double v : xs) s += v;
-  return s / static_cast<double>(xs.size());
-}
+double mean(std::span<const double> xs) { return moments(xs, false).mean; }
 
-double sample_stddev(std::span<const double> xs) {
-  if (xs.size() < 2) throw InsufficientDataError("stddev needs at least 2 observations");
-  const double mu = mean(xs);
-  double ss = 0.0;
-  for (double v : xs) ss += (v - mu) * (v - mu);
-  return std::sqrt(ss / static_cast<double>(xs.size() - 1));
-}
+double sample_stddev(std::span<const double> xs) { return stddev_of(moments(xs, true)); }
 
+// 0.975 quantile of Student's t with df degrees of freedom (Boost-free):
+// the two-sided 5 % tail solves I_x(df/2, 1/2) = 0.05 at x = df/(df + t^2),
+// and I is increasing in x, so x is bisected to the last representable step.
 double t_quantile_975(int df) {
-  if (df < 1) throw InsufficientDataError("t quantile needs df >= 1");
+  if (df < 1) throw InsufficientDataError("the t quantile needs one or more degrees of freedom");
   const double a = 0.5 * static_cast<double>(df);
-  // Two-sided tail 0.05: find x in (0,1) with I_x(a, 1/2) = 0.05; I is increasing in x.
   double lo = 0.0, hi = 1.0;
   for (int it = 0; it < 200; ++it) {
     const double mid = 0.5 * (lo + hi);
     if (mid <= lo || mid >= hi) break;
-    if (reg_inc_beta(a, 0.5, mid) < 0.05)
-      lo = mid;
-    else
-      hi = mid;
+    (reg_inc_beta(a, 0.5, mid) < 0.05 ? lo : hi) = mid;
   }
   const double x = 0.5 * (lo + hi);
   return std::sqrt(static_cast<double>(df) * (1.0 - x) / x);
 }
 
 double ci_halfwidth95(std::span<const double> xs) {
-  if (xs.size() < 2) throw InsufficientDataError("confidence interval needs >= 2 observations");
-  const double n = static_cast<double>(xs.size());
-  return t_quantile_975(static_cast<int>(xs.size()) - 1) * sample_stddev(xs) / std::sqrt(n);
+  const Moments m = moments(xs, true);
+  return t_quantile_975(static_cast<int>(m.n) - 1) * stddev_of(m) / std::sqrt(static_cast<double>(m.n));
 }
 
 Summary summarize(std::span<const double> xs) {
-  Summary s;
-  s.count = static_cast<int>(xs.size());
-  s.mean = mean(xs);
-  s.stddev = sample_stddev(xs);
-  s.ci_halfwidth = ci_halfwidth95(xs);
-  return s;
+  const Moments m = moments(xs, true);
+  const double sd = stddev_of(m);
+  return Summary{static_cast<int>(m.n), m.mean, sd,
+                 t_quantile_975(static_cast<int>(m.n) - 1) * sd / std::sqrt(static_cast<double>(m.n))};
 }
 
 }  // namespace imb

@@ -66,19 +66,21 @@ def test_paper_worked_example():
 def test_live_random_parity_against_compiled_reference():
     from oracle import oracle as O
     rng = random.Random(77)
-    for _ in range(300):
-        g = rng.choice([1, 2, 3])
-        x = rng.randint(1, 3) * g
+    for _ in range(1500):
+        g = rng.choice([1, 2, 3, 4])
+        x = rng.randint(1, 4) * g
         samples = []
-        for _ in range(rng.randint(2, 7)):
-            samples.append((x, rng.choice([rng.uniform(1, 9), float(rng.randint(1, 6))])))
-            x += rng.randint(1, 2) * g
-        total = rng.randint(1, 30) * g
-        p = rng.randint(1, 4)
+        for _ in range(rng.randint(1, 10)):
+            # integer speeds make ties (and equal makespans) common
+            samples.append((x, rng.choice([rng.uniform(1, 9), float(rng.randint(1, 4))])))
+            x += rng.randint(1, 3) * g
+        total = rng.randint(1, 40) * g
+        p = rng.randint(1, 6)
         idle = rng.random() < 0.3
+        unit = rng.choice([1, 7, 15360])
         for kind in ("paired", "general", "brute"):
-            st, sh, pt, ms, off = O.ref_partition(kind, 1, g, samples, total, p, idle)
-            mst, r = product(kind, 1, g, samples, total, p, idle)
+            st, sh, pt, ms, off = O.ref_partition(kind, unit, g, samples, total, p, idle)
+            mst, r = product(kind, unit, g, samples, total, p, idle)
             assert mst == st, (kind, samples, total, p, idle)
             if st == 0:
                 assert (r.shares, r.per_time, r.makespan, r.offset) == (sh, pt, ms, off)
