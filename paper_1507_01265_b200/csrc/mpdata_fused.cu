@@ -4,27 +4,38 @@
 // fluxes) lives in shared memory or registers.
 //
 // Geometry (B200-first):
-//  * A warp owns whole rows: each lane holds KPT = l/32 CONSECUTIVE k values
-//    of a row (l in {32, 64, 128}), so every global/shared access is a
-//    16/32-byte vector per lane and a warp moves a whole contiguous row; the
-//    k +- 1 neighbours are in-register or one warp shuffle away, with the
-//    periodic k wrap closing inside the warp (no k halo, no k-neighbour loads).
+//  * A warp owns whole rows. A lane holds E = NS*K cells of a row: NS
+//    segments of K consecutive k (segment sg covers k in [sg*32K, (sg+1)*32K),
+//    lane l its cells sg*32K + l*K + [0, K)). Every global/shared access is a
+//    16-byte vector per lane and segment, so a warp moves a whole contiguous
+//    row with conflict-free shared-memory wavefronts (fp64 at l = 128 uses
+//    2 segments of 2 doubles). The k +- 1 neighbours are in registers or one
+//    warp shuffle away: lane 0 of segment sg takes its k - 1 from lane 31 of
+//    segment sg - 1 — the value the shuffle of that segment already delivers
+//    to lane 0 — so the periodic k wrap and the segment seams close inside
+//    the warp with a select, never with a reload.
 //  * A block owns a j-tile of TJ output rows plus a recomputed halo of 2 rows
 //    (limiter) or 1 row (plain) on each side: RR = NW*RW region rows.
 //  * The block streams along i (the slab axis) over a segment of planes. The
 //    stages run one plane apart, so along i nothing is recomputed except a
-//    two-plane warm-up per segment. Shared memory holds 3 planes of psi^(1),
-//    2 of the y/z pseudo-velocities and 2 of each beta; same-column
-//    dependencies along i (x-face velocity, x-flux, the psi^n star extrema)
-//    are register carries.
+//    two-plane warm-up per segment. Shared memory holds the psi^(1) planes,
+//    the y/z pseudo-velocities and both betas of the planes in flight;
+//    same-column dependencies along i (x-face velocity, x-flux, the psi^n
+//    star extrema) are register carries.
+//  * Addressing: every global address is one 32-bit element index (plane
+//    offset + row offset + lane offset, the row offsets loop-invariant)
+//    scaled into the field pointer by a single IMAD.WIDE, with the segment
+//    offsets as load immediates — no 64-bit multiplies in the stream loop.
+//    The fused path therefore needs fields of < 2^32 elements (checked by
+//    fused_supported's caller through FusedShape).
 //  * Inputs come through L1/L2 (warp 0 bulk-prefetches every plane into L2
 //    one plane ahead). fp32 at l = 128 also stages psi^n and h, the two most
 //    re-read fields, in shared-memory rings filled by bulk async copies (TMA
 //    engine, one mbarrier per slot); fp64 has no shared memory left for it.
 //  * Divisions: fp64 folds the four divisions of a pseudo-velocity into one
-//    reciprocal of hb*dA*dB*dC and the two beta divisions into one, with a
-//    MUFU seed + 2 Newton steps; fp32 uses MUFU.RCP. Both stay inside the
-//    parity tolerance (1e-12 / 1e-5).
+//    reciprocal of hb*dA*dB*dC and the two beta divisions into one (MUFU seed
+//    + one cubic Newton step); fp32 divides exactly (div.rn) and is compiled
+//    without FMA contraction, so it rounds like the oracle (mpdata_math.cuh).
 // The per-cell arithmetic follows SURVEY.md Appendix A (see mpdata_math.cuh).
 #include <cuda_runtime.h>
 
@@ -58,12 +69,6 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_ACC(slot, a, b)
 #endif
 
-#ifndef IMB_EARLY_DONOR
-#define IMB_EARLY_DONOR 1
-#endif
-#ifndef IMB_EARLY_STARC
-#define IMB_EARLY_STARC 1
-#endif
 #ifndef IMB_TWO_F32  // two barriers per plane (see Cfg::TWO): fp32 +7.6 % C4, +4 % C5
 #define IMB_TWO_F32 1
 #endif
@@ -71,22 +76,21 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_TWO_F64 0
 #endif
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR = 1, bool STG = false>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false>
 struct Cfg {
-  // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
-  static constexpr int KPT = L / (32 * NS * WPR);  // consecutive k per lane and segment
-  static_assert(KPT * 32 * NS * WPR == L, "row must split into warp-wide segments");
-  static_assert(WPR == 1 || RW == 1, "several warps per row take one row each");
-  static constexpr int RR = NW * RW / WPR;         // region rows
-  static constexpr int HALO = NONOS ? 2 : 1;      // recomputed rows on each side
-  static constexpr int TJ = RR - 2 * HALO;        // output rows per tile
+  static constexpr int KPT = L / (32 * NS);  // consecutive k per lane and segment
+  static_assert(KPT * 32 * NS == L, "row must split into warp-wide segments");
+  static constexpr int E = NS * KPT;         // cells of a row per lane
+  static constexpr int SEG = 32 * KPT;       // cells per segment
+  static constexpr int RR = NW * RW;         // region rows
+  static constexpr int HALO = NONOS ? 2 : 1; // recomputed rows on each side
+  static constexpr int TJ = RR - 2 * HALO;   // output rows per tile
   static constexpr int NT = NW * 32;
-  static constexpr int PLANE = RR * L;            // cells of one smem plane
+  static constexpr int PLANE = RR * L;       // cells of one smem plane
   // EARLY: the donor of plane t+3 runs in the same barrier phase as the
   // limiter/final update of plane t (3 barriers per plane instead of 4),
-  // which takes a 4th psi^(1) slot. The STARC (register-carried psi^n star)
-  // variants keep the donor in its own phase.
-  static constexpr bool EARLY = NONOS && IMB_EARLY_DONOR && L == 128;  // l=64: measured -3.5%
+  // which takes a 4th psi^(1) slot.
+  static constexpr bool EARLY = NONOS && L == 128;  // l=64: measured -3.5%
   static constexpr int NX1 = EARLY ? 4 : 3;  // psi^(1) slots
   // TWO: the donor of plane t+3 runs with the bounds (phase 2) and the
   // barrier between the final update (phase 3) and the next plane's
@@ -140,21 +144,87 @@ struct Args {
   int push_sys;  // push targets may be on a peer GPU (system-scope fence)
 };
 
+// ---- k +- 1 neighbours of a lane's segment vector ---------------------------
+// A warp holds NS segments of 32*K consecutive k of a row; inside a segment
+// the neighbour is one shuffle away, and with NS == 1 the shuffle also
+// closes the periodic wrap. With NS > 1 lane 0 (31) reloads its single
+// neighbour across the seam: p is this lane's first cell of the segment
+// (the offset folds into the load's immediate once the segment loop is
+// unrolled), and the predicated load writes the shuffle's register in place
+// (no merge moves).
+template <int L, int NS, bool GLOBAL, class T, int K>
+__device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, const T* p, int sg, int lane) {
+  Vec<T, K> r;
+  r.e[0] = __shfl_sync(kFull, a.e[K - 1], (lane + 31) & 31);
+  if constexpr (NS > 1) {
+    static_assert(sizeof(T) == 8, "seam reloads are written for fp64");
+    const T* q = p + (sg == 0 ? L - 1 : -1);  // lane 0's neighbour (sg is unrolled: an immediate)
+    if constexpr (GLOBAL)
+      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 0;\n\t@q ld.global.nc.f64 %0, [%2];\n\t}"
+          : "+d"(r.e[0]) : "r"(lane), "l"(q));
+    else
+      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 0;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
+          : "+d"(r.e[0]) : "r"(lane), "r"(static_cast<unsigned>(__cvta_generic_to_shared(q))));
+  }
+#pragma unroll
+  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
+  return r;
+}
+template <int L, int NS, bool GLOBAL, class T, int K>
+__device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, const T* p, int sg, int lane) {
+  Vec<T, K> r;
+  r.e[K - 1] = __shfl_sync(kFull, a.e[0], (lane + 1) & 31);
+  if constexpr (NS > 1) {
+    static_assert(sizeof(T) == 8, "seam reloads are written for fp64");
+    // p is this lane's first cell of the segment; lane 31 needs the cell
+    // after the segment (the next segment's first, or k = 0 after the last)
+    const T* q = p + (sg == NS - 1 ? K - L : K);
+    if constexpr (GLOBAL)
+      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 31;\n\t@q ld.global.nc.f64 %0, [%2];\n\t}"
+          : "+d"(r.e[K - 1]) : "r"(lane), "l"(q));
+    else
+      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 31;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
+          : "+d"(r.e[K - 1]) : "r"(lane), "r"(static_cast<unsigned>(__cvta_generic_to_shared(q))));
+  }
+#pragma unroll
+  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
+  return r;
+}
+// Shared-memory rows with one segment (fp32): the single out-of-vector
+// neighbour is re-read from the row (p = this lane's first cell; the wrap is
+// in the offset).
+template <int L, class T, int K>
+__device__ __forceinline__ Vec<T, K> kminus_s(const Vec<T, K>& a, const T* p, int lane) {
+  Vec<T, K> r;
+  r.e[0] = p[lane == 0 ? L - 1 : -1];
+#pragma unroll
+  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
+  return r;
+}
+template <int L, class T, int K>
+__device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int lane) {
+  Vec<T, K> r;
+  r.e[K - 1] = p[lane == 31 ? K - L : K];
+#pragma unroll
+  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
+  return r;
+}
+
 // MODE 0: one IORD=2 step. MODE 1: donor + first corrective pass of an
 // IORD=3 step, additionally writing the pass's limited velocities and 7-point
 // bounds. MODE 2: the second corrective pass from psi^(2) (read instead of the
 // donor), the limited velocities (as u, v, w) and the accumulated bounds.
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, int WPR, bool STG>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS, WPR, STG>;
-  static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && WPR == 1 && C::EARLY),
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG>;
+  static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && C::EARLY),
                 "staged inputs: IORD=2 limiter, one row per warp");
-  constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS;
+  constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS, SEG = 32 * K;
   using V = Vec<T, K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  T* s_x1 = sm;                          // 3 slots of psi^(1), by plane mod 3
-  constexpr bool EARLY = C::EARLY && (!STARC || IMB_EARLY_STARC);
+  T* s_x1 = sm;                          // psi^(1) slots, by plane
+  constexpr bool EARLY = C::EARLY;
   T* s_v = sm + C::NX1 * PL;             // y-face pseudo-velocities
   T* s_w = s_v + C::NVW * PL;            // z-face pseudo-velocities
   T* s_bu = s_w + C::NVW * PL;           // beta up,   2 slots (NONOS)
@@ -181,44 +251,61 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #ifdef IMB_CHECK_SELFTEST  // proves a failing assert traps (tools/checked_build.sh --selftest)
   IMB_ASSERT(blockIdx.x != 0 || threadIdx.x != 0, "selftest", 0);
 #endif
-  const int wrow = (warp / WPR) * RW;        // first region row of this warp
-  const int wcol = (warp % WPR) * (L / WPR);  // first k of this warp's row part
+  const int wrow = warp * RW;  // first region row of this warp
+  const int lk = lane * K;     // this lane's first k of segment 0
+  const unsigned PLN = static_cast<unsigned>(a.plane);
 
-  // Rows of this warp: region row r = warp*RW + rr; global row offsets (j
-  // wraps periodically) of the row and its j-1 / j+1 neighbours.
-  int gj[RW], gjm[RW], gjp[RW];
+  // Rows of this warp: region row r = wrow + rr. Element offsets within a
+  // plane of this lane's first cell in the row and in its j-1 / j+1
+  // neighbours (j wraps periodically) — loop-invariant.
+  unsigned gj[RW], gjm[RW], gjp[RW];
 #pragma unroll
   for (int rr = 0; rr < RW; ++rr) {
     int j = j0 - C::HALO + wrow + rr;
     j = ((j % m) + m) % m;
-    gj[rr] = j * L;
-    gjm[rr] = (j == 0 ? m - 1 : j - 1) * L;
     IMB_ASSERT(j >= 0 && j < m, "row outside the plane", j);
-    gjp[rr] = (j == m - 1 ? 0 : j + 1) * L;
+    gj[rr] = static_cast<unsigned>(j * L + lk);
+    gjm[rr] = static_cast<unsigned>((j == 0 ? m - 1 : j - 1) * L + lk);
+    gjp[rr] = static_cast<unsigned>((j == m - 1 ? 0 : j + 1) * L + lk);
   }
   auto slot3 = [](int p) { return C::NX1 == 4 ? ((p + 8) & 3) : (p + 6) % 3; };  // p >= -3
-  auto pl = [&](int p) {
+  // element offset of plane p of the padded slab
+  auto pl = [&](int p) -> unsigned {
     IMB_ASSERT(p + a.R >= 0 && p < a.ni + a.R, "plane outside the padded slab", p);
-    return static_cast<long long>(p + a.R) * a.plane;
+    return static_cast<unsigned>(p + a.R) * PLN;
   };
+  // cell group c = (row rr, segment sg): this lane's first cell of the
+  // segment relative to its first cell of the row
+  auto sgo = [](int c) { return (c % NS) * SEG; };
+  // k +- 1 of a global row (p = this lane's cell pointer of the segment) or
+  // of a shared row (fp64 shuffles, fp32 re-reads the out-of-vector value:
+  // +1.4 % C4, +1 % C2 over shuffles)
+  constexpr bool SRL = sizeof(T) == 4 && NS == 1;
+#define KMG(c, vec, p) kminus<L, NS, true>(vec, p, (c) % NS, lane)
+#define KPG(c, vec, p) kplus<L, NS, true>(vec, p, (c) % NS, lane)
+#define KMS(c, vec, p) (SRL ? kminus_s<L>(vec, p, lane) : kminus<L, NS, false>(vec, p, (c) % NS, lane))
+#define KPS(c, vec, p) (SRL ? kplus_s<L>(vec, p, lane) : kplus<L, NS, false>(vec, p, (c) % NS, lane))
+
   // STG rings: psi^n planes from xb = ib - 3, h planes from hb = ib - 2 (the
   // first each warm-up donor reads); slot and fill (mbarrier phase) by plane.
   const int xb = ib - 3, hb = ib - 2;
   auto xslot = [&](int q) { return (q - xb) & (C::NXS - 1); };
   auto hslot = [&](int q) { return (q - hb) % C::NHS; };
-  auto xrow = [&](int q, int r) { return s_xs + (xslot(q) * C::XROWS + r + 1) * L; };
-  auto hrow = [&](int q, int r) { return s_hs + (hslot(q) * C::HROWS + r) * L; };
+  // this lane's first cell of region row r in the staged rings
+  auto xrow = [&](int q, int r) { return s_xs + (xslot(q) * C::XROWS + r + 1) * L + lk; };
+  auto hrow = [&](int q, int r) { return s_hs + (hslot(q) * C::HROWS + r) * L + lk; };
   const int jstage = j0 - C::HALO;  // global row of region row 0
   // one thread: rows jfirst.. of plane q of field f (periodic in j) -> dst
   auto stage_rows = [&](T* dst, const T* f, int q, int jfirst, int nrows, unsigned long long* bar) {
     const unsigned bytes = static_cast<unsigned>(nrows * L * sizeof(T));
     mbar_expect_tx(bar, bytes);
-    const T* base = f + pl(q);
+    const unsigned base = pl(q);
     const int j = ((jfirst % m) + m) % m;
     const int first = j + nrows <= m ? nrows : m - j;
-    bulk_g2s(dst, base + static_cast<long long>(j) * L, static_cast<unsigned>(first * L * sizeof(T)), bar);
+    bulk_g2s(dst, f + (base + static_cast<unsigned>(j * L)),
+             static_cast<unsigned>(first * L * sizeof(T)), bar);
     if (first < nrows)
-      bulk_g2s(dst + first * L, base, static_cast<unsigned>((nrows - first) * L * sizeof(T)), bar);
+      bulk_g2s(dst + first * L, f + base, static_cast<unsigned>((nrows - first) * L * sizeof(T)), bar);
   };
   auto fill_x = [&](int q) {
     stage_rows(s_xs + xslot(q) * C::XROWS * L, a.x, q, jstage - 1, C::XROWS, &mbar[xslot(q)]);
@@ -244,8 +331,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       for (int q = ib - 2; q <= ib + 1; ++q) fill_h(q);
     }
   }
-  // cell group c = (row rr, segment sg): first k of this lane in the segment
-  auto k0of = [&](int c) { return wcol + (c % NS) * 32 * K + lane * K; };
   // MODE 1: plane t+1 values of an own tile row are stored once (segments
   // abut: this block owns planes [ib, ie), the last segment also plane o1).
   auto keep = [&](int t, int r) {
@@ -257,21 +342,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // j-neighbour warps through shared-memory progress counters — was measured
   // 3-4x slower than the hardware barrier and removed.)
   auto nb_sync = [&]() { __syncthreads(); };
-  // neighbour helpers: G = global source row, S = shared source row
-#define KMG(vec, row, k0) kminus<L, NS * WPR, true>(vec, row, k0, lane)
-#define KPG(vec, row, k0) kplus<L, NS * WPR, true>(vec, row, k0, lane)
-  // k+-1 of a shared-memory row: fp64 shuffles (smem reloads measured -3 % C4,
-  // -6 % C2), fp32 re-reads the one out-of-vector value from the row (+1.4 % C4,
-  // +1 % C2 over shuffles).
-#ifndef IMB_SMEM_RELOAD
-  constexpr bool SRL = sizeof(T) == 4;
-#else
-  constexpr bool SRL = true;
-#endif
-#define KMS(vec, row, k0) \
-  (SRL ? kminus_s<L>(vec, row, k0) : kminus<L, NS * WPR, false>(vec, row, k0, lane))
-#define KPS(vec, row, k0) \
-  (SRL ? kplus_s<L>(vec, row, k0) : kplus<L, NS * WPR, false>(vec, row, k0, lane))
 
   // psi^n star extrema (STARC): of plane t+1 (nmx), t+2 (nmx_mid, EARLY) and
   // the donor's newest plane (nmx_new)
@@ -279,29 +349,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 
   // P1: psi^(1) at plane p (donor cell) for all region rows.
   auto stage_donor = [&](int p) {
-    const T* X = a.x + pl(p);
-    const T* Xm = a.x + pl(p - 1);
-    const T* Xp = a.x + pl(p + 1);
-    const T* U = a.u + pl(p);
-    const T* Up = a.u + pl(p + 1);
-    const T* Vv = a.v + pl(p);
-    const T* W = a.w + pl(p);
-    const T* H = a.h + pl(p);
+    const unsigned px = pl(p);
     T* dst = s_x1 + slot3(p) * PL;
     if constexpr (MODE == 2) {  // psi^(2) is an input: stage it, carry the bounds
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        const int rr = c / NS, k0 = k0of(c);
-        const int g = gj[rr] + k0;
-        vstore(dst + (wrow + rr) * L + k0, vload<T, K>(X + g));
+        const int rr = c / NS, so = sgo(c);
+        const unsigned ij = px + gj[rr];
+        vstore(dst + (wrow + rr) * L + lk + so, vload<T, K>(a.x + ij + so));
         if constexpr (STARC) {
-          nmx_new[c] = vload<T, K>(a.mxo + pl(p) + g);
-          nmn_new[c] = vload<T, K>(a.mno + pl(p) + g);
+          nmx_new[c] = vload<T, K>(a.mxo + ij + so);
+          nmn_new[c] = vload<T, K>(a.mno + ij + so);
         }
       }
       return;
     }
-    const int nc_donor = MODE == 2 ? 0 : NC;  // (MODE 2 returned above)
     if constexpr (STG) {
       // donors run in plane order: the older two psi^n planes were waited
       // for by the previous donor (all three by the segment's first)
@@ -313,35 +375,37 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       wait_h(p);
     }
 #pragma unroll
-    for (int c = 0; c < nc_donor; ++c) {
-      const int rr = c / NS, k0 = k0of(c);
+    for (int c = 0; c < NC; ++c) {
+      const int rr = c / NS, so = sgo(c);
       const int r = wrow + rr;
-      const int g = gj[rr] + k0;
+      const unsigned ij = px + gj[rr];
+      const T* X = a.x + ij + so;
       V xc, xm, xp, ym, yp, zm, zp, hc;
       if constexpr (STG) {
-        const T* xr = xrow(p, r);
-        xc = sload<T, K>(xr + k0);
-        xm = sload<T, K>(xrow(p - 1, r) + k0);
-        xp = sload<T, K>(xrow(p + 1, r) + k0);
-        ym = sload<T, K>(xr - L + k0);
-        yp = sload<T, K>(xr + L + k0);
-        zm = KMS(xc, xr, k0);
-        zp = KPS(xc, xr, k0);
-        hc = sload<T, K>(hrow(p, r) + k0);
+        const T* xr = xrow(p, r) + so;
+        xc = sload<T, K>(xr);
+        xm = sload<T, K>(xrow(p - 1, r) + so);
+        xp = sload<T, K>(xrow(p + 1, r) + so);
+        ym = sload<T, K>(xr - L);
+        yp = sload<T, K>(xr + L);
+        zm = KMS(c, xc, xr);
+        zp = KPS(c, xc, xr);
+        hc = sload<T, K>(hrow(p, r) + so);
       } else {
-        xc = vload<T, K>(X + g);
-        xm = vload<T, K>(Xm + g);
-        xp = vload<T, K>(Xp + g);
-        ym = vload<T, K>(X + gjm[rr] + k0);
-        yp = vload<T, K>(X + gjp[rr] + k0);
-        zm = KMG(xc, X + gj[rr], k0);
-        zp = KPG(xc, X + gj[rr], k0);
-        hc = vload<T, K>(H + g);
+        xc = vload<T, K>(X);
+        xm = vload<T, K>(a.x + (ij - PLN) + so);
+        xp = vload<T, K>(a.x + (ij + PLN) + so);
+        ym = vload<T, K>(a.x + (px + gjm[rr]) + so);
+        yp = vload<T, K>(a.x + (px + gjp[rr]) + so);
+        zm = KMG(c, xc, X);
+        zp = KPG(c, xc, X);
+        hc = vload<T, K>(a.h + ij + so);
       }
-      const V uc = vload<T, K>(U + g), up = vload<T, K>(Up + g);
-      const V vc = vload<T, K>(Vv + g), vp = vload<T, K>(Vv + gjp[rr] + k0);
-      const V wc = vload<T, K>(W + g);
-      const V wp = KPG(wc, W + gj[rr], k0);
+      const V uc = vload<T, K>(a.u + ij + so), up = vload<T, K>(a.u + (ij + PLN) + so);
+      const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
+      const T* W = a.w + ij + so;
+      const V wc = vload<T, K>(W);
+      const V wp = KPG(c, wc, W);
       V res;
 #pragma unroll
       for (int e = 0; e < K; ++e) {
@@ -361,7 +425,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
                                  tmin(tmin(yp.e[e], zm.e[e]), zp.e[e]));
         }
       }
-      vstore(dst + r * L + k0, res);
+      vstore(dst + r * L + lk + so, res);
     }
   };
 
@@ -371,33 +435,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     const T* s0 = s_x1 + slot3(pb - 1) * PL;
     const T* s1 = s_x1 + slot3(pb) * PL;
     const T* s2 = s_x1 + slot3(pb + 1) * PL;
-    const T* U1 = a.u + pl(pb);
-    const T* U2 = a.u + pl(pb + 1);
-    const T* V1 = a.v + pl(pb);
-    const T* V2 = a.v + pl(pb + 1);
-    const T* W1 = a.w + pl(pb);
-    const T* W2 = a.w + pl(pb + 1);
-    const T* H1 = a.h + pl(pb);
-    const T* H2 = a.h + pl(pb + 1);
+    const unsigned p1 = pl(pb), p2 = p1 + PLN;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      const int rr = c / NS, k0 = k0of(c);
+      const int rr = c / NS, sg = sgo(c);
       const int r = wrow + rr;
       if (r < 1) continue;  // warp-uniform
       const bool row_u = r < RR - 1;  // x/z faces (y faces: every r >= 1)
-      const int g = gj[rr] + k0;
-      const int so = r * L + k0;  // smem offset of this vector
+      const unsigned i1 = p1 + gj[rr], i2 = p2 + gj[rr];
+      const int so = r * L + lk + sg;  // smem offset of this vector
       const V x1 = sload<T, K>(s1 + so);
       const V a1 = vabs(x1);
       const V a1m = vabs(sload<T, K>(s1 + so - L));
-      const V u2c = vload<T, K>(U2 + g);
-      const V h1c = STG ? sload<T, K>(hrow(pb, r) + k0) : vload<T, K>(H1 + g);
-      const V a1km = vabs(KMS(x1, s1 + r * L, k0));
+      const T* U2 = a.u + i2 + sg;
+      const V u2c = vload<T, K>(U2);
+      const V h1c = STG ? sload<T, K>(hrow(pb, r) + sg) : vload<T, K>(a.h + i1 + sg);
+      const V a1km = vabs(KMS(c, x1, s1 + so));
       if (row_u) {  // x-face between planes pb and pb+1 of this column
         const V x2 = sload<T, K>(s2 + so);
         const V a2 = vabs(x2);
-        const V a1kp = vabs(KPS(x1, s1 + r * L, k0));
-        const V a2kp = vabs(KPS(x2, s2 + r * L, k0)), a2km = vabs(KMS(x2, s2 + r * L, k0));
+        const V a1kp = vabs(KPS(c, x1, s1 + so));
+        const V a2kp = vabs(KPS(c, x2, s2 + so)), a2km = vabs(KMS(c, x2, s2 + so));
         V bp, bm, cp, cm, Vs, Ws;
         {
           const V a1p = vabs(sload<T, K>(s1 + so + L)), a2p = vabs(sload<T, K>(s2 + so + L));
@@ -411,18 +469,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
         }
         {
-          const V v1 = vload<T, K>(V1 + g), v2 = vload<T, K>(V2 + g);
-          const V v1p = vload<T, K>(V1 + gjp[rr] + k0), v2p = vload<T, K>(V2 + gjp[rr] + k0);
+          const V v1 = vload<T, K>(a.v + i1 + sg), v2 = vload<T, K>(a.v + i2 + sg);
+          const V v1p = vload<T, K>(a.v + (p1 + gjp[rr]) + sg), v2p = vload<T, K>(a.v + (p2 + gjp[rr]) + sg);
 #pragma unroll
           for (int e = 0; e < K; ++e) Vs.e[e] = (v1.e[e] + v2.e[e]) + (v1p.e[e] + v2p.e[e]);
         }
         {
-          const V w1 = vload<T, K>(W1 + g), w2 = vload<T, K>(W2 + g);
-          const V w1p = KPG(w1, W1 + gj[rr], k0), w2p = KPG(w2, W2 + gj[rr], k0);
+          const T* W1 = a.w + i1 + sg;
+          const T* W2 = a.w + i2 + sg;
+          const V w1 = vload<T, K>(W1), w2 = vload<T, K>(W2);
+          const V w1p = KPG(c, w1, W1), w2p = KPG(c, w2, W2);
 #pragma unroll
           for (int e = 0; e < K; ++e) Ws.e[e] = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
         }
-        const V h2 = STG ? sload<T, K>(hrow(pb + 1, r) + k0) : vload<T, K>(H2 + g);
+        const V h2 = STG ? sload<T, K>(hrow(pb + 1, r) + sg) : vload<T, K>(a.h + i2 + sg);
 #pragma unroll
         for (int e = 0; e < K; ++e)
           ut[c].e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e], bp.e[e],
@@ -431,16 +491,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (only_u) continue;
       const V x0 = sload<T, K>(s0 + so);
       const V x2 = sload<T, K>(s2 + so);
-      const V u1c = vload<T, K>(U1 + g);
-      const V w1 = vload<T, K>(W1 + g);
+      const T* U1 = a.u + i1 + sg;
+      const V u1c = vload<T, K>(U1);
+      const T* W1 = a.w + i1 + sg;
+      const V w1 = vload<T, K>(W1);
       {  // y-face between rows r-1 and r of plane pb
         const V x1m = sload<T, K>(s1 + so - L);
         V bp, bm, cp, cm, Us, Ws;
         {
           const V a0m = vabs(sload<T, K>(s0 + so - L)), a2m = vabs(sload<T, K>(s2 + so - L));
-          const V a1mkp = vabs(KPS(x1m, s1 + (r - 1) * L, k0));
-          const V a1mkm = vabs(KMS(x1m, s1 + (r - 1) * L, k0));
-          const V a1kp = vabs(KPS(x1, s1 + r * L, k0));
+          const V a1mkp = vabs(KPS(c, x1m, s1 + so - L));
+          const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
+          const V a1kp = vabs(KPS(c, x1, s1 + so));
 #pragma unroll
           for (int e = 0; e < K; ++e) {
             bp.e[e] = a2m.e[e] + fabs(x2.e[e]);
@@ -450,18 +512,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
         }
         {
-          const V u1m = vload<T, K>(U1 + gjm[rr] + k0), u2m = vload<T, K>(U2 + gjm[rr] + k0);
+          const V u1m = vload<T, K>(a.u + (p1 + gjm[rr]) + sg), u2m = vload<T, K>(a.u + (p2 + gjm[rr]) + sg);
 #pragma unroll
           for (int e = 0; e < K; ++e) Us.e[e] = (u1m.e[e] + u1c.e[e]) + (u2m.e[e] + u2c.e[e]);
         }
         {
-          const V w1m = vload<T, K>(W1 + gjm[rr] + k0);
-          const V w1mkp = KPG(w1m, W1 + gjm[rr], k0), w1kp = KPG(w1, W1 + gj[rr], k0);
+          const T* W1m = a.w + (p1 + gjm[rr]) + sg;
+          const V w1m = vload<T, K>(W1m);
+          const V w1mkp = KPG(c, w1m, W1m), w1kp = KPG(c, w1, W1);
 #pragma unroll
           for (int e = 0; e < K; ++e) Ws.e[e] = (w1m.e[e] + w1.e[e]) + (w1mkp.e[e] + w1kp.e[e]);
         }
-        const V v1 = vload<T, K>(V1 + g);
-        const V h1m = STG ? sload<T, K>(hrow(pb, r - 1) + k0) : vload<T, K>(H1 + gjm[rr] + k0);
+        const V v1 = vload<T, K>(a.v + i1 + sg);
+        const V h1m = STG ? sload<T, K>(hrow(pb, r - 1) + sg) : vload<T, K>(a.h + (p1 + gjm[rr]) + sg);
         V res;
 #pragma unroll
         for (int e = 0; e < K; ++e)
@@ -474,9 +537,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         {
           const V x1p = sload<T, K>(s1 + so + L);
           const V x1m = sload<T, K>(s1 + so - L);
-          const V a1pkm = vabs(KMS(x1p, s1 + (r + 1) * L, k0));
-          const V a1mkm = vabs(KMS(x1m, s1 + (r - 1) * L, k0));
-          const V a2km = vabs(KMS(x2, s2 + r * L, k0)), a0km = vabs(KMS(x0, s0 + r * L, k0));
+          const V a1pkm = vabs(KMS(c, x1p, s1 + so + L));
+          const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
+          const V a2km = vabs(KMS(c, x2, s2 + so)), a0km = vabs(KMS(c, x0, s0 + so));
 #pragma unroll
           for (int e = 0; e < K; ++e) {
             bp.e[e] = a2km.e[e] + fabs(x2.e[e]);
@@ -486,17 +549,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
         }
         {
-          const V u2km = KMG(u2c, U2 + gj[rr], k0), u1km = KMG(u1c, U1 + gj[rr], k0);
+          const V u2km = KMG(c, u2c, U2), u1km = KMG(c, u1c, U1);
 #pragma unroll
           for (int e = 0; e < K; ++e) Us.e[e] = (u1km.e[e] + u1c.e[e]) + (u2km.e[e] + u2c.e[e]);
         }
         {
-          const V v1 = vload<T, K>(V1 + g), v1p = vload<T, K>(V1 + gjp[rr] + k0);
-          const V v1km = KMG(v1, V1 + gj[rr], k0), v1pkm = KMG(v1p, V1 + gjp[rr], k0);
+          const T* V1 = a.v + i1 + sg;
+          const T* V1p = a.v + (p1 + gjp[rr]) + sg;
+          const V v1 = vload<T, K>(V1), v1p = vload<T, K>(V1p);
+          const V v1km = KMG(c, v1, V1), v1pkm = KMG(c, v1p, V1p);
 #pragma unroll
           for (int e = 0; e < K; ++e) Vs.e[e] = (v1km.e[e] + v1.e[e]) + (v1pkm.e[e] + v1p.e[e]);
         }
-        const V h1km = STG ? KMS(h1c, hrow(pb, r), k0) : KMG(h1c, H1 + gj[rr], k0);
+        const V h1km = STG ? KMS(c, h1c, hrow(pb, r) + sg) : KMG(c, h1c, a.h + i1 + sg);
         V res;
 #pragma unroll
         for (int e = 0; e < K; ++e)
@@ -577,12 +642,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const int p = t + lag + 1 + a.pf;
       if (p <= ie + lag && p < a.ni + a.R) {
         const T* f = lane == 0 ? a.x : lane == 1 ? a.u : lane == 2 ? a.v : lane == 3 ? a.w : a.h;
-        const T* base = f + pl(p);
+        const unsigned base = pl(p);
         int j = pf_j < 0 ? pf_j + m : pf_j;
         const int first = (j + pf_rows <= m) ? pf_rows : m - j;
-        l2_prefetch(base + static_cast<long long>(j) * L, static_cast<unsigned>(first * L * sizeof(T)));
+        l2_prefetch(f + (base + static_cast<unsigned>(j * L)), static_cast<unsigned>(first * L * sizeof(T)));
         if (first < pf_rows)
-          l2_prefetch(base, static_cast<unsigned>((pf_rows - first) * L * sizeof(T)));
+          l2_prefetch(f + base, static_cast<unsigned>((pf_rows - first) * L * sizeof(T)));
       }
     }
     IMB_T(0)
@@ -618,34 +683,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const T* s0 = s_x1 + slot3(t) * PL;
         const T* s1 = s_x1 + slot3(t + 1) * PL;
         const T* s2 = s_x1 + slot3(t + 2) * PL;
-        const T* H1 = a.h + pl(p1);
-        const T* Xn0 = a.x + pl(t);
-        const T* Xn1 = a.x + pl(p1);
-        const T* Xn2 = a.x + pl(t + 2);
+        const unsigned q1 = pl(p1);
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          const int rr = c / NS, k0 = k0of(c);
+          const int rr = c / NS, sg = sgo(c);
           const int r = wrow + rr;
           if (r < 1 || r >= RR - 1) continue;
-          const int so = r * L + k0;
+          const int so = r * L + lk + sg;
+          const unsigned i1 = q1 + gj[rr];
           const V xc = sload<T, K>(s1 + so);
           const V xm = sload<T, K>(s0 + so), xp = sload<T, K>(s2 + so);
           const V ym = sload<T, K>(s1 + so - L), yp = sload<T, K>(s1 + so + L);
-          const V zm = KMS(xc, s1 + r * L, k0), zp = KPS(xc, s1 + r * L, k0);
+          const V zm = KMS(c, xc, s1 + so), zp = KPS(c, xc, s1 + so);
           V mx, mn;
           if constexpr (STARC) {
             mx = nmx[c];
             mn = nmn[c];
           } else if constexpr (MODE == 2) {  // bounds of the previous pass
-            const int g = gj[rr] + k0;
-            mx = vload<T, K>(a.mxo + pl(p1) + g);
-            mn = vload<T, K>(a.mno + pl(p1) + g);
+            mx = vload<T, K>(a.mxo + i1 + sg);
+            mn = vload<T, K>(a.mno + i1 + sg);
           } else {  // psi^n star of plane t+1, reloaded
-            const int g = gj[rr] + k0;
-            const V nc = vload<T, K>(Xn1 + g);
-            const V n0 = vload<T, K>(Xn0 + g), n2 = vload<T, K>(Xn2 + g);
-            const V nym = vload<T, K>(Xn1 + gjm[rr] + k0), nyp = vload<T, K>(Xn1 + gjp[rr] + k0);
-            const V nzm = KMG(nc, Xn1 + gj[rr], k0), nzp = KPG(nc, Xn1 + gj[rr], k0);
+            const T* N = a.x + i1 + sg;
+            const V nc = vload<T, K>(N);
+            const V n0 = vload<T, K>(a.x + (i1 - PLN) + sg), n2 = vload<T, K>(a.x + (i1 + PLN) + sg);
+            const V nym = vload<T, K>(a.x + (q1 + gjm[rr]) + sg), nyp = vload<T, K>(a.x + (q1 + gjp[rr]) + sg);
+            const V nzm = KMG(c, nc, N), nzp = KPG(c, nc, N);
 #pragma unroll
             for (int e = 0; e < K; ++e) {
               mx.e[e] = tmax(tmax(tmax(nc.e[e], n0.e[e]), tmax(n2.e[e], nym.e[e])),
@@ -656,8 +718,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
           const V va = sload<T, K>(vA + so), vap = sload<T, K>(vA + so + L);
           const V wa = sload<T, K>(wA + so);
-          const V wap = KPS(wa, wA + r * L, k0);
-          const V hc = STG ? sload<T, K>(hrow(p1, r) + k0) : vload<T, K>(H1 + gj[rr] + k0);
+          const V wap = KPS(c, wa, wA + so);
+          const V hc = STG ? sload<T, K>(hrow(p1, r) + sg) : vload<T, K>(a.h + i1 + sg);
           V bu, bd, his, los;
 #pragma unroll
           for (int e = 0; e < K; ++e) {
@@ -696,8 +758,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           vstore(bdA + so, bd);
           if constexpr (MODE == 1) {  // bounds for the next pass
             if (keep(t, r)) {
-              vstore(a.mxo + pl(p1) + gj[rr] + k0, his);
-              vstore(a.mno + pl(p1) + gj[rr] + k0, los);
+              vstore(a.mxo + i1 + sg, his);
+              vstore(a.mno + i1 + sg, los);
             }
           }
         }
@@ -714,14 +776,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       {
         const T* s0 = s_x1 + slot3(t) * PL;
         const T* s1 = s_x1 + slot3(t + 1) * PL;
-        const T* H0 = a.h + pl(t);
-        T* O = a.out + pl(t);
+        const unsigned q0 = pl(t), q1 = q0 + PLN;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          const int rr = c / NS, k0 = k0of(c);
+          const int rr = c / NS, sg = sgo(c);
           const int r = wrow + rr;
           if (r < 2 || r >= RR - 1) continue;
-          const int so = r * L + k0;
+          const int so = r * L + lk + sg;
           const V bu = sload<T, K>(buA + so), bd = sload<T, K>(bdA + so);
           {
             const V va = sload<T, K>(vA + so);
@@ -732,14 +793,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               res.e[e] = limit_sel(va.e[e], bdm.e[e], bu.e[e], bum.e[e], bd.e[e]);
             vstore(vA + so, res);
             if constexpr (MODE == 1) {
-              if (keep(t, r)) vstore(a.vo + pl(p1) + gj[rr] + k0, res);
+              if (keep(t, r)) vstore(a.vo + (q1 + gj[rr]) + sg, res);
             }
           }
           if (r >= RR - 2) continue;
           V fxr;
           {
             const V wa = sload<T, K>(wA + so);
-            const V bukm = KMS(bu, buA + r * L, k0), bdkm = KMS(bd, bdA + r * L, k0);
+            const V bukm = KMS(c, bu, buA + so), bdkm = KMS(c, bd, bdA + so);
             const V buo = sload<T, K>(buB + so), bdo = sload<T, K>(bdB + so);
             const V xc = sload<T, K>(s0 + so);
             const V x1 = sload<T, K>(s1 + so);
@@ -754,19 +815,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             vstore(wA + so, wres);
             if constexpr (MODE == 1) {
               if (keep(t, r)) {
-                vstore(a.wo + pl(p1) + gj[rr] + k0, wres);
-                vstore(a.uo + pl(p1) + gj[rr] + k0, uls);
+                vstore(a.wo + (q1 + gj[rr]) + sg, wres);
+                vstore(a.uo + (q1 + gj[rr]) + sg, uls);
               }
             }
           }
           if (emit) {
             const V xc = sload<T, K>(s0 + so);
             const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
-            const V zm = KMS(xc, s0 + r * L, k0), zp = KPS(xc, s0 + r * L, k0);
+            const V zm = KMS(c, xc, s0 + so), zp = KPS(c, xc, s0 + so);
             const V vb = sload<T, K>(vB + so), vbp = sload<T, K>(vB + so + L);
             const V wb = sload<T, K>(wB + so);
-            const V wbp = KPS(wb, wB + r * L, k0);
-            const V hc = STG ? sload<T, K>(hrow(t, r) + k0) : vload<T, K>(H0 + gj[rr] + k0);
+            const V wbp = KPS(c, wb, wB + so);
+            const V hc = STG ? sload<T, K>(hrow(t, r) + sg) : vload<T, K>(a.h + (q0 + gj[rr]) + sg);
             V res;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
@@ -779,7 +840,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               res.e[e] = x0 - qdiv(div, hc.e[e]);
             }
             const int j = j0 + r - 2;
-            if (j < m) vstore(O + gj[rr] + k0, res);
+            if (j < m) vstore(a.out + (q0 + gj[rr]) + sg, res);
           }
           fxc[c] = fxr;
         }
@@ -814,22 +875,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const T* sm1 = s_x1 + slot3(t - 1) * PL;
       const T* s0 = s_x1 + slot3(t) * PL;
       const T* s1 = s_x1 + slot3(t + 1) * PL;
-      const T* H0 = a.h + pl(t);
-      T* O = a.out + pl(t);
+      const unsigned q0 = pl(t);
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        const int rr = c / NS, k0 = k0of(c);
+        const int rr = c / NS, sg = sgo(c);
         const int r = wrow + rr;
         if (r < 1 || r >= RR - 1) continue;
-        const int so = r * L + k0;
+        const int so = r * L + lk + sg;
         const V xc = sload<T, K>(s0 + so);
         const V xm = sload<T, K>(sm1 + so), xp = sload<T, K>(s1 + so);
         const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
-        const V zm = KMS(xc, s0 + r * L, k0), zp = KPS(xc, s0 + r * L, k0);
+        const V zm = KMS(c, xc, s0 + so), zp = KPS(c, xc, s0 + so);
         const V vv = sload<T, K>(s_v + so), vvp = sload<T, K>(s_v + so + L);
         const V ww = sload<T, K>(s_w + so);
-        const V wwp = KPS(ww, s_w + r * L, k0);
-        const V hc = vload<T, K>(H0 + gj[rr] + k0);
+        const V wwp = KPS(c, ww, s_w + so);
+        const V hc = vload<T, K>(a.h + (q0 + gj[rr]) + sg);
         V res;
 #pragma unroll
         for (int e = 0; e < K; ++e) {
@@ -844,7 +904,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           res.e[e] = x0 - qdiv(div, hc.e[e]);
         }
         const int j = j0 + r - 1;
-        if (j < m) vstore(O + gj[rr] + k0, res);
+        if (j < m) vstore(a.out + (q0 + gj[rr]) + sg, res);
         ucar[c] = ufresh[c];
       }
       nb_sync();
@@ -864,19 +924,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         T* dstb = pass == 0 ? a.push_lo : a.push_hi;
         if (dstb == nullptr) continue;
         for (int t = p0; t < p1; ++t) {
-          const long long dplane = pass == 0 ? static_cast<long long>(a.R + a.lo_ni + t)
-                                             : static_cast<long long>(a.R + t - a.ni);
+          const int dplane = pass == 0 ? a.R + a.lo_ni + t : a.R + t - a.ni;
+          IMB_ASSERT(pass == 0 ? (dplane >= a.lo_ni + a.R && dplane < a.lo_ni + 2 * a.R)
+                               : (dplane >= 0 && dplane < a.R),
+                     "halo push plane", dplane);
+          const unsigned dbase = static_cast<unsigned>(dplane) * PLN;
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-            const int rr = c / NS, k0 = k0of(c);
+            const int rr = c / NS, sg = sgo(c);
             const int r = wrow + rr;
             if (r < C::HALO || r >= RR - C::HALO || j0 + r - C::HALO >= m) continue;
-            const int g = gj[rr] + k0;
             // L2-coherent load: a.out was written by this kernel
-            IMB_ASSERT(pass == 0 ? (dplane >= a.lo_ni + a.R && dplane < a.lo_ni + 2 * a.R)
-                                 : (dplane >= 0 && dplane < a.R),
-                       "halo push plane", dplane);
-            vstore(dstb + dplane * a.plane + g, vload_cg<T, K>(a.out + pl(t) + g));
+            vstore(dstb + (dbase + gj[rr]) + sg, vload_cg<T, K>(a.out + (pl(t) + gj[rr]) + sg));
           }
         }
       }
@@ -899,6 +958,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 // resident slot that frees first; a block costs its planes + the warm-up);
 // the smallest makespan wins, then the fewest blocks. Uniform splits are the
 // candidates with no remainder. Plans are cached per shape.
+#ifndef IMB_ONLY_F32  // precision-independent host code lives in the fp64 object
 Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int warm) {
   static std::mutex mu;
   static std::map<std::tuple<std::int64_t, int, std::int64_t, int, int>, Plan> cache;
@@ -936,14 +996,14 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   cache.emplace(key, best);
   return best;
 }
+#endif
 
 namespace {
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, int WPR = 1,
-          bool STG = false>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG = false>
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS, WPR, STG>;
-  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, WPR, STG>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG>;
+  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG>;
   // Function attributes and occupancy are per device: configure each device
   // once (a group or a measurement may drive several GPUs from one process).
   static std::mutex mu;
@@ -997,36 +1057,6 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
   constexpr bool D = sizeof(T) == 8;
   switch (fs.l) {
     case 128:
-#ifdef IMB_FUSED_VARIANTS
-      if (std::getenv("IMB_WPR2"))  // 32 warps, 2 per row, 2 x 32 cells each
-        return launch_cfg<T, 128, 1, 32, 2, NONOS, false, MODE, 2>(fs, a, num_sms, st);
-      if (const char* e = std::getenv("IMB_RWV")) {  // two rows per warp, bigger tiles
-        const int v = std::atoi(e);
-        if (v == 1) return launch_cfg<T, 128, 2, 10, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (v == 2) return launch_cfg<T, 128, 2, 10, 2, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (v == 3) return launch_cfg<T, 128, 2, 8, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (v == 4) return launch_cfg<T, 128, 2, 8, 2, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (v == 7) return launch_cfg<T, 128, 2, 10, 1, NONOS, true, MODE>(fs, a, num_sms, st);
-        if (v == 8) return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, false, MODE>(fs, a, num_sms, st);
-        if (v == 9) return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, true, MODE>(fs, a, num_sms, st);
-        if (v == 10) return launch_cfg<T, 128, 1, 16, 1, NONOS, false, MODE>(fs, a, num_sms, st);
-        if (v == 11) return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE>(fs, a, num_sms, st);
-        if (v == 12) return launch_cfg<T, 128, 1, 16, 4, NONOS, false, MODE>(fs, a, num_sms, st);
-        if (v == 13) return launch_cfg<T, 128, 1, 16, 2, NONOS, true, MODE>(fs, a, num_sms, st);
-        if (v == 14) return launch_cfg<T, 128, 1, 16, 2, NONOS, false, MODE>(fs, a, num_sms, st);
-        if constexpr (!D) {
-          if (v == 5) return launch_cfg<T, 128, 2, 16, 1, NONOS, true, MODE>(fs, a, num_sms, st);
-          if (v == 6) return launch_cfg<T, 128, 2, 12, 1, NONOS, true, MODE>(fs, a, num_sms, st);
-        }
-      }
-      if (const char* e = std::getenv("IMB_NW")) {  // fewer region rows, more registers
-        const int nw = std::atoi(e);
-        if (nw == 14) return launch_cfg<T, 128, 1, 14, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (nw == 15) return launch_cfg<T, 128, 1, 15, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (nw == 12) return launch_cfg<T, 128, 1, 12, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
-        if (nw == 20) return launch_cfg<T, 128, 1, 20, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
-      }
-#endif
       if constexpr (!D && NONOS && MODE != 2) {
         // psi^n and h staged by bulk async copies: C4 fp32 +3.3 %, C5 fp32 +1 %
         // (IMB_STG=0 turns it off for A/B runs)
@@ -1035,7 +1065,7 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
           return !(e && e[0] == '0');
         }();
         if (stg && fs.m >= 18)
-          return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE, 1, true>(fs, a, num_sms, st);
+          return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE, true>(fs, a, num_sms, st);
       }
       return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
@@ -1046,12 +1076,16 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
 
 }  // namespace
 
-bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool) {
-  const bool shape = (l == 32 || l == 64 || l == 128) && m >= 3 && m < (1 << 20);
+#ifndef IMB_ONLY_F32
+bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, std::int64_t planes) {
+  // the kernel addresses every field with 32-bit element indices
+  const bool fits = planes > 0 && planes * m * l < (std::int64_t{1} << 32);
+  const bool shape = (l == 32 || l == 64 || l == 128) && m >= 3 && m < (1 << 20) && fits;
   return shape && (iord == 2 || (iord == 3 && nonos));
 }
+#endif
 
-#ifdef IMB_PHASE_TIMING
+#if defined(IMB_PHASE_TIMING) && !defined(IMB_ONLY_F32)
 extern "C" int imb_debug_phase_cycles(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
   if (reset) {
@@ -1094,19 +1128,30 @@ int launch_fused3(const FusedShape& fs, const T* x, const T* u, const T* v, cons
   return n2 < 0 ? n2 : n + n2;
 }
 
+// Each precision is its own object (Makefile): fp32 is built with
+// --fmad=false so it rounds exactly like the oracle (mpdata_math.cuh).
+#ifndef IMB_ONLY_F32
 template int launch_fused<double>(const FusedShape&, int, int, const double*, const double*,
                                   const double*, const double*, const double*, double*, int,
                                   cudaStream_t, const HaloPush<double>&);
+#endif
+#ifndef IMB_ONLY_F64
 template int launch_fused<float>(const FusedShape&, int, int, const float*, const float*,
                                  const float*, const float*, const float*, float*, int,
                                  cudaStream_t, const HaloPush<float>&);
+#endif
+#ifndef IMB_ONLY_F32
 template int launch_fused3<double>(const FusedShape&, const double*, const double*, const double*,
                                    const double*, const double*, double*, double*, double*,
                                    double*, double*, double*, double*, int, cudaStream_t,
                                    const HaloPush<double>&);
+#endif
+#ifndef IMB_ONLY_F64
 template int launch_fused3<float>(const FusedShape&, const float*, const float*, const float*,
                                   const float*, const float*, float*, float*, float*, float*,
                                   float*, float*, float*, int, cudaStream_t,
                                   const HaloPush<float>&);
+
+#endif
 
 }  // namespace imb::dev

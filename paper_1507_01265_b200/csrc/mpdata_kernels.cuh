@@ -64,8 +64,9 @@ struct Plan {
   int ntj, kseg, lseg, blocks;
 };
 Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int warm);
-// True when the fused kernel supports this (iord, nonos, m, l) combination.
-bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, bool fp64);
+// True when the fused kernel supports this (iord, nonos, m, l) combination on
+// a padded slab of `planes` planes (its fields are indexed with 32 bits).
+bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, std::int64_t planes);
 template <class T>
 int launch_fused(const FusedShape& fs, int iord, int nonos, const T* x, const T* u, const T* v,
                  const T* w, const T* h, T* out, int num_sms, cudaStream_t st,

@@ -263,8 +263,14 @@ int launch_limit(const Span& s, T* ut, T* vt, T* wt, const T* bu, const T* bd, c
   template int launch_beta<T>(const Span&, const T*, const T*, const T*, const T*, const T*,     \
                               const T*, const T*, T*, T*, cudaStream_t);                         \
   template int launch_limit<T>(const Span&, T*, T*, T*, const T*, const T*, cudaStream_t);
+// Each precision is its own object (Makefile): fp32 is built with
+// --fmad=false so it rounds exactly like the oracle (mpdata_math.cuh).
+#ifndef IMB_ONLY_F32
 IMB_INSTANTIATE(double)
+#endif
+#ifndef IMB_ONLY_F64
 IMB_INSTANTIATE(float)
+#endif
 #undef IMB_INSTANTIATE
 
 }  // namespace imb::dev

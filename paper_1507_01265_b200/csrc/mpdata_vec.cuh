@@ -1,7 +1,6 @@
-// Per-lane vectors of K consecutive k values and their load/store/neighbour
-// helpers, shared by the fused streaming kernels (mpdata_fused.cu,
-// mpdata_split.cu). A warp holds NS segments of 32*K cells of a row; k +- 1
-// neighbours are in-register or one shuffle away (see kminus/kplus).
+// Per-lane vectors of K consecutive k values and their load/store helpers,
+// plus the mbarrier / bulk-copy wrappers of the fused streaming kernel
+// (mpdata_fused.cu holds the k +- 1 neighbour helpers).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -174,58 +173,6 @@ __device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or
   }
 }
 
-// Value at k-1 / k+1 of a lane vector. The warp holds NS consecutive
-// segments of 32*K cells per row; inside a segment the neighbour is one
-// shuffle away, and with NS == 1 the shuffle also closes the periodic k wrap.
-// With NS > 1 the segment-edge lane reloads its single neighbour from the
-// vector's source row (global read-only path when G, shared memory else).
-template <int L, int NS, bool G, class T, int K>
-__device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, const T* row, int k0, int lane) {
-  Vec<T, K> r;
-  r.e[0] = __shfl_sync(kFull, a.e[K - 1], (lane + 31) & 31);
-  if constexpr (NS > 1) {
-    if (lane == 0) {
-      const T* p = row + (k0 == 0 ? L - 1 : k0 - 1);
-      r.e[0] = G ? __ldg(p) : *p;
-    }
-  }
-#pragma unroll
-  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
-  return r;
-}
-template <int L, int NS, bool G, class T, int K>
-__device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, const T* row, int k0, int lane) {
-  Vec<T, K> r;
-  r.e[K - 1] = __shfl_sync(kFull, a.e[0], (lane + 1) & 31);
-  if constexpr (NS > 1) {
-    if (lane == 31) {
-      const T* p = row + (k0 + K == L ? 0 : k0 + K);
-      r.e[K - 1] = G ? __ldg(p) : *p;
-    }
-  }
-#pragma unroll
-  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
-  return r;
-}
-// k-1 / k+1 of a vector held in shared memory: the single out-of-vector
-// element is read back from the row (periodic wrap in the address), so no
-// shuffle and no edge-lane special case.
-template <int L, class T, int K>
-__device__ __forceinline__ Vec<T, K> kminus_s(const Vec<T, K>& a, const T* row, int k0) {
-  Vec<T, K> r;
-  r.e[0] = row[k0 == 0 ? L - 1 : k0 - 1];
-#pragma unroll
-  for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
-  return r;
-}
-template <int L, class T, int K>
-__device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* row, int k0) {
-  Vec<T, K> r;
-  r.e[K - 1] = row[k0 + K == L ? 0 : k0 + K];
-#pragma unroll
-  for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
-  return r;
-}
 template <class T, int K>
 __device__ __forceinline__ Vec<T, K> vabs(const Vec<T, K>& a) {
   Vec<T, K> r;

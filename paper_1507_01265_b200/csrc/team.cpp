@@ -202,7 +202,7 @@ void Team::acquire() {
   const std::size_t fbytes = static_cast<std::size_t>(P_) * plane_bytes();
   // The fused kernels take any slab >= R planes (they read R halo planes);
   // every slab of a decomposition then runs the same arithmetic.
-  const bool fused = dev::fused_supported(opt_.iord, opt_.nonos, m_, l_, opt_.fp64);
+  const bool fused = dev::fused_supported(opt_.iord, opt_.nonos, m_, l_, P_);
   const int ntmp = fused ? 0 : 12;
   const int next = (fused && opt_.iord == 3) ? 6 : 0;  // psi^(2), bounds, limited velocities
   const std::size_t total = fbytes * static_cast<std::size_t>(7 + ntmp + next);
