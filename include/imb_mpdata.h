@@ -195,6 +195,21 @@ int imb_average(int64_t unit_cells, int64_t granularity, const imb_speed_sample*
 int imb_scaled(int64_t unit_cells, int64_t granularity, const imb_speed_sample* s, int ns,
                double factor, imb_speed_sample* out);
 
+/* Speed-function CSV (the "# unit_cells=.. granularity=..
+ * label=.." header, then x,speed,ci_halfwidth,repetitions rows, doubles at
+ * %.17g). The one parser/writer of the format (csrc/host/fpm.cpp); the
+ * Python mirror and the CLI go through these.
+ * parse: up to `cap` samples into out, *ns = the sample count (call with
+ * cap = 0 to size), label copied NUL-terminated into label[label_cap];
+ * IMB_E_PARSE with the 1-based line in *err_line (0 otherwise).
+ * format: the text into out[cap] (NUL-terminated), *len = its length
+ * without the NUL; IMB_E_RANGE when cap is too small (*len says how much). */
+int imb_speed_csv_parse(const char* text, size_t len, int64_t* unit_cells, int64_t* granularity,
+                        imb_speed_sample* out, int cap, int* ns, char* label, size_t label_cap,
+                        int* err_line);
+int imb_speed_csv_format(int64_t unit_cells, int64_t granularity, const imb_speed_sample* s,
+                         int ns, const char* label, char* out, size_t cap, size_t* len);
+
 /* slice_surface, fpm.hpp:123 (+ SpeedSurface::validate, fpm.hpp:81-91): the
  * surface is nn x nm samples, row-major in n (samples[i*nm + j].x must equal
  * m_values[j]); out receives the nm samples of row fixed_n and

@@ -109,6 +109,10 @@ SIGNATURES = {
     "imb_classify_shape": (i32, [i64, i64, SS, i32, P(i32), P(i64)]),
     "imb_average": (i32, [i64, i64, SS, i32, i32, SS]),
     "imb_scaled": (i32, [i64, i64, SS, i32, f64, SS]),
+    "imb_speed_csv_parse": (i32, [C.c_char_p, C.c_size_t, P(i64), P(i64), SS, i32, P(i32), C.c_char_p,
+                                  C.c_size_t, P(i32)]),
+    "imb_speed_csv_format": (i32, [i64, i64, SS, i32, C.c_char_p, C.c_char_p, C.c_size_t,
+                                   P(C.c_size_t)]),
     "imb_slice_surface": (i32, [i64, i64, P(i64), i32, P(i64), i32, SS, i64, SS, P(i64)]),
     "imb_predict_makespan": (i32, [i64, i64, SS, i32, P(i64), i32, P(f64), P(f64)]),
     "imb_partition_paired": (i32, [i64, i64, SS, i32, i64, i32, i32, P(i64), P(f64), P(f64), P(i64)]),

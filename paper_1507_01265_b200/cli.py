@@ -203,6 +203,49 @@ def measure_simultaneous(ni, m, l, opts, devices, steps, ci, min_reps, max_reps,
     return sums, len(times[0]), conv
 
 
+def measure_ring(ni, m, l, opts, devices, steps, ci, min_reps, max_reps, warmup, seed):
+    """The production halo path: the listed devices form one ring of slabs of
+    ni planes each (an in-process group, the decomposition of a
+    len(devices)*ni-plane grid), so every team's time includes its halo push
+    into its neighbours (over NVLink between GPUs) and the step
+    synchronisation. Each team's time is its own device compute time per step
+    (the group's event windows). A device id may repeat: p
+    slabs sharing one GPU is the labelled single-GPU stand-in.
+    -> ([Summary], reps, converged)"""
+    from . import mpdata
+    nt = len(devices)
+    times = [[] for _ in range(nt)]
+    g = mpdata.Group(ni * nt, m, l, [ni] * nt, devices=devices, opts=opts)
+    try:
+        g.init_recipe(mpdata.RECIPE_ROTCUBE, seed)
+        if warmup:
+            g.run(warmup)
+        while True:
+            per, _ = g.run(steps)
+            for q in range(nt):
+                times[q].append(per[q] / steps)
+            n = len(times[0])
+            if n >= max_reps:
+                break
+            if n >= min_reps:
+                sums = [fpm.summarize(ts) for ts in times]
+                if all(s.ci_halfwidth <= ci * s.mean for s in sums):
+                    break
+    finally:
+        g.close()
+    sums = [fpm.summarize(ts) for ts in times]
+    conv = all(s.ci_halfwidth <= ci * s.mean for s in sums)
+    return sums, len(times[0]), conv
+
+
+def halo_label(args, devices):
+    if args.halo == "self":
+        return "halo=self (periodic single slab per GPU)"
+    shared = len(set(devices)) < len(devices)
+    return (f"halo=ring p={len(devices)} devices={','.join(map(str, devices))}"
+            + (" (slabs share a GPU: stand-in)" if shared else ""))
+
+
 def cmd_measure(args) -> int:
     xs = parse_range(args.x)
     gran = int(args.x.split(":")[2])
@@ -219,46 +262,53 @@ def cmd_measure(args) -> int:
     if xs[0] < R:
         raise UsageError(f"slab thickness {xs[0]} is below the step radius {R}")
     l = args.l
-    per = {d: {} for d in devices}  # device -> {(m, x): SpeedSample}
+    if args.halo == "self" and len(set(devices)) < len(devices):
+        raise UsageError("--halo self needs distinct --devices (repeat a device only with --halo ring)")
+    def tname(q):  # gpu<id> for distinct devices, team<q> when slabs share a GPU
+        return f"gpu{devices[q]}" if len(set(devices)) == len(devices) else f"team{q}"
+
+    per = {d: {} for d in range(len(devices))}  # team -> {(m, x): SpeedSample}
     unconverged = []
     for m in ms:
         for x in xs:
-            sums, reps, conv = measure_simultaneous(x, m, l, opts, devices, args.steps, args.ci,
-                                                    args.min_reps, args.max_reps, args.warmup,
-                                                    args.seed)
+            how = measure_ring if args.halo == "ring" else measure_simultaneous
+            sums, reps, conv = how(x, m, l, opts, devices, args.steps, args.ci, args.min_reps,
+                                   args.max_reps, args.warmup, args.seed)
             if not conv:
                 unconverged.append([m, x])
-            for d, s in zip(devices, sums):
+            for q, s in enumerate(sums):
                 speed = x * m * l / s.mean  # cell-updates per second
-                per[d][(m, x)] = fpm.SpeedSample(x, speed, speed * s.ci_halfwidth / s.mean, reps)
+                per[q][(m, x)] = fpm.SpeedSample(x, speed, speed * s.ci_halfwidth / s.mean, reps)
             if not args.json:
                 print(f"m={m} x={x}: " + "  ".join(
-                    f"gpu{d} {x * m * l / s.mean / 1e9:.3f} Gcell/s" for d, s in zip(devices, sums)),
+                    f"{tname(q)} {x * m * l / s.mean / 1e9:.3f} Gcell/s" for q, s in enumerate(sums)),
                     flush=True)
     prec = "fp32" if args.fp32 else "fp64"
-    what = f"iord{opts.iord}{' nonos' if opts.nonos else ''} {prec} l={l} cell-updates/s per step"
+    what = (f"iord{opts.iord}{' nonos' if opts.nonos else ''} {prec} l={l} cell-updates/s per step "
+            f"{halo_label(args, devices)}")
     files = []
 
-    def one_d(d, m, label):
-        return fpm.SpeedFunction(m * l, gran, tuple(per[d][(m, x)] for x in xs), label)
+    def one_d(q, m, label):
+        return fpm.SpeedFunction(m * l, gran, tuple(per[q][(m, x)] for x in xs), label)
 
     if len(ms) == 1:  # speed functions: x = slab planes, unit = one m x l plane
         m = ms[0]
-        fs = [one_d(d, m, f"gpu{d} m={m} {what}") for d in devices]
-        for d, f in zip(devices, fs):
-            files.append(write_out(args, f"speed_gpu{d}.csv", fpm.write_csv(f)))
+        fs = [one_d(q, m, f"{tname(q)} m={m} {what}") for q in range(len(devices))]
+        for q, f in enumerate(fs):
+            files.append(write_out(args, f"speed_{tname(q)}.csv", fpm.write_csv(f)))
         avg = fpm.average(fs)
         files.append(write_out(args, "speed_avg.csv", fpm.write_csv(avg)))
         files.append(write_out(args, "speed_avg.dat", "".join(
             f"{s.x} {s.speed:.17g}\n" for s in avg.samples)))
     else:  # surface keyed by (n = rows m, m = slab planes x); unit = one row of l cells
-        for d in devices:
-            smp = [per[d][(m, x)] for m in ms for x in xs]
-            files.append(write_out(args, f"surface_gpu{d}.csv", fpm.write_surface_csv(
-                fpm.SpeedSurface(l, gran, tuple(ms), tuple(xs), tuple(smp), f"gpu{d} {what}"))))
+        for q in range(len(devices)):
+            smp = [per[q][(m, x)] for m in ms for x in xs]
+            files.append(write_out(args, f"surface_{tname(q)}.csv", fpm.write_surface_csv(
+                fpm.SpeedSurface(l, gran, tuple(ms), tuple(xs), tuple(smp), f"{tname(q)} {what}"))))
         avg_smp = []
         for m in ms:
-            fs = [fpm.SpeedFunction(l, gran, tuple(per[d][(m, x)] for x in xs)) for d in devices]
+            fs = [fpm.SpeedFunction(l, gran, tuple(per[q][(m, x)] for x in xs))
+                  for q in range(len(devices))]
             avg_smp += list(fpm.average(fs).samples)
         files.append(write_out(args, "surface_avg.csv", fpm.write_surface_csv(
             fpm.SpeedSurface(l, gran, tuple(ms), tuple(xs), tuple(avg_smp),
@@ -266,6 +316,7 @@ def cmd_measure(args) -> int:
     man = manifest(args)
     man["outputs"] = [str(p) for p in files]
     man["unconverged"] = unconverged
+    man["halo"] = halo_label(args, devices)
     files.append(write_out(args, "measure_manifest.json", json.dumps(man, indent=1) + "\n"))
     emit(args, man, "wrote " + ", ".join(str(p) for p in files)
          + (f"\nunconverged (m, x): {unconverged}" if unconverged else ""))
@@ -337,7 +388,11 @@ def cmd_validate(args) -> int:
              write_out(args, "table1.dat", "".join(f"{r['offset']} {r['t_exp_s']:.9g}\n"
                                                     for r in rows))]
     man = manifest(args, [args.model])
-    man.update(mode="lockstep decomposition" if lockstep else "per-share timing on one GPU",
+    mode = "per-share timing on one GPU"
+    if lockstep:
+        mode = ("lockstep decomposition" if len(set(devices[:p])) == p else
+                "lockstep decomposition (slabs share a GPU: stand-in)")
+    man.update(mode=mode, halo="ring (kernel halo push between slabs)" if lockstep else "self",
                table1=rows, table2=teams, outputs=[str(q) for q in files])
     files.append(write_out(args, "validate_manifest.json", json.dumps(man, indent=1) + "\n"))
     text = f"{'offset':>6} {'t_theory':>10} {'t_exp':>10} {'speedup':>8} {'err':>7}\n" + "".join(
@@ -383,6 +438,10 @@ def build_parser() -> argparse.ArgumentParser:
     work.add_argument("--warmup", type=int, default=1)
     work.add_argument("--ci", type=float, default=0.05, help="target CI half-width / mean")
     work.add_argument("--max-reps", type=int, default=20)
+    work.add_argument("--halo", choices=["self", "ring"], default="self",
+                      help="measure: 'self' = one periodic slab per GPU; 'ring' = the listed "
+                           "devices form one slab ring with the production halo push (a "
+                           "device may repeat: slabs sharing a GPU, a labelled stand-in)")
 
     ap = argparse.ArgumentParser(prog="imbalance", description=__doc__.split("\n")[0])
     sub = ap.add_subparsers(dest="cmd", required=True)

@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <exception>
+#include <sstream>
 #include <memory>
 #include <new>
 #include <string>
@@ -511,6 +513,55 @@ int imb_scaled(int64_t unit, int64_t g, const imb_speed_sample* s, int ns, doubl
       const imb::SpeedSample& v = a.samples()[static_cast<std::size_t>(q)];
       out[q] = imb_speed_sample{v.x, v.speed, v.ci_halfwidth, v.repetitions};
     }
+  });
+}
+
+int imb_speed_csv_parse(const char* text, size_t len, int64_t* unit_cells, int64_t* granularity,
+                        imb_speed_sample* out, int cap, int* ns, char* label, size_t label_cap,
+                        int* err_line) {
+  if (err_line) *err_line = 0;
+  try {
+    need(text, "text");
+    need(ns, "ns");
+    std::istringstream is(std::string(text, len));
+    const imb::SpeedFunction f = imb::read_speed_function_csv(is);
+    const auto& sm = f.samples();
+    *ns = static_cast<int>(sm.size());
+    if (cap > 0) need(out, "out");
+    for (int q = 0; q < cap && q < *ns; ++q)
+      out[q] = imb_speed_sample{sm[q].x, sm[q].speed, sm[q].ci_halfwidth, sm[q].repetitions};
+    if (unit_cells) *unit_cells = f.unit_cells();
+    if (granularity) *granularity = f.granularity();
+    if (label && label_cap > 0) {
+      const std::size_t n = std::min(label_cap - 1, f.label().size());
+      std::memcpy(label, f.label().data(), n);
+      label[n] = '\0';
+    }
+    return IMB_OK;
+  } catch (const imb::ParseError& e) {
+    if (err_line) *err_line = e.line;
+    return guard([&] { throw; });
+  } catch (...) {
+    return guard([&] { throw; });
+  }
+}
+
+int imb_speed_csv_format(int64_t unit_cells, int64_t granularity, const imb_speed_sample* s,
+                         int ns, const char* label, char* out, size_t cap, size_t* len) {
+  return guard([&] {
+    need(len, "len");
+    std::vector<imb::SpeedSample> v;
+    if (ns > 0) need(s, "samples");
+    for (int q = 0; q < ns; ++q) v.push_back({s[q].x, s[q].speed, s[q].ci_halfwidth, s[q].repetitions});
+    const imb::SpeedFunction f(unit_cells, granularity, std::move(v), label ? label : "");
+    std::ostringstream os;
+    imb::write_speed_function_csv(os, f);
+    const std::string t = os.str();
+    *len = t.size();
+    if (cap < t.size() + 1) throw imb::RangeError("output buffer too small for the CSV text");
+    need(out, "out");
+    std::memcpy(out, t.data(), t.size());
+    out[t.size()] = '\0';
   });
 }
 

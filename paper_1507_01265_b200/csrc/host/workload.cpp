@@ -142,6 +142,31 @@ void upload_field(rt::Team& t, int id, const GridField& f, bool fp64) {
   }
 }
 
+// A reference caller loops over run_step, so the device team (padded-slab
+// buffers, streams, events) is cached per host thread and reused while the
+// domain and options stay the same; only the five fields move per call.
+rt::Team& step_team(const StencilDomain& d, const MpdataOptions& o) {
+  struct Cached {
+    std::int64_t n = 0, m = 0, l = 0;
+    int iord = 0;
+    bool nonos = false, fp64 = false;
+    std::unique_ptr<rt::Team> team;
+  };
+  thread_local Cached c;
+  if (!c.team || c.n != d.n || c.m != d.m || c.l != d.l || c.iord != o.iord || c.nonos != o.nonos ||
+      c.fp64 != o.fp64) {
+    c.team.reset();  // free the old buffers before allocating the new ones
+    c.team = std::make_unique<rt::Team>(d.n, d.m, d.l, to_rt(o), 0, 0, d.n);
+    c.n = d.n;
+    c.m = d.m;
+    c.l = d.l;
+    c.iord = o.iord;
+    c.nonos = o.nonos;
+    c.fp64 = o.fp64;
+  }
+  return *c.team;
+}
+
 }  // namespace
 
 GridField run_step(const InputFields& fields, const StencilDomain& domain,
@@ -149,7 +174,7 @@ GridField run_step(const InputFields& fields, const StencilDomain& domain,
   domain.validate();
   for (const GridField* g : {&fields.x, &fields.u, &fields.v, &fields.w, &fields.rho})
     if (!g->halo_valid) throw ContractError("run_step input halo is not filled");
-  rt::Team team(domain.n, domain.m, domain.l, to_rt(opts), 0, 0, domain.n);
+  rt::Team& team = step_team(domain, opts);
   upload_field(team, 0, fields.x, opts.fp64);
   upload_field(team, 1, fields.u, opts.fp64);
   upload_field(team, 2, fields.v, opts.fp64);

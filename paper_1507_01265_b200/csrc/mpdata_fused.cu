@@ -76,13 +76,13 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_TWO_F64 0
 #endif
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false, int WPR = 1>
 struct Cfg {
-  static constexpr int KPT = L / (32 * NS);  // consecutive k per lane and segment
-  static_assert(KPT * 32 * NS == L, "row must split into warp-wide segments");
-  static constexpr int E = NS * KPT;         // cells of a row per lane
-  static constexpr int SEG = 32 * KPT;       // cells per segment
-  static constexpr int RR = NW * RW;         // region rows
+  // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
+  static constexpr int KPT = L / (32 * NS * WPR);  // consecutive k per lane and segment
+  static_assert(KPT * 32 * NS * WPR == L, "row must split into warp-wide segments");
+  static_assert(WPR == 1 || RW == 1, "several warps per row take one row each");
+  static constexpr int RR = NW * RW / WPR;   // region rows
   static constexpr int HALO = NONOS ? 2 : 1; // recomputed rows on each side
   static constexpr int TJ = RR - 2 * HALO;   // output rows per tile
   static constexpr int NT = NW * 32;
@@ -210,14 +210,75 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
   return r;
 }
 
+#ifndef IMB_TMEM_STAR  // psi^n star extrema carried in tensor memory (fp64, see k_fused)
+#define IMB_TMEM_STAR 1
+#endif
+#ifndef IMB_TMEM_CACHE  // h and v rows cached in tensor memory across iterations (fp64)
+#define IMB_TMEM_CACHE 1
+#endif
+
+// ---- tensor memory (TMEM) as per-thread storage ------------------------------
+// The stencil has no MMA, so the SM's 256 KB of TMEM is free: a warp reads
+// and writes its own 32-lane quarter (lane = thread), 512 32-bit columns per
+// lane shared by the NW/4 warps of that quarter. LDTM returns in ~12 cycles
+// against several hundred for an L2 hit.
+[[maybe_unused]] __device__ __forceinline__ void tmem_ld8(unsigned taddr, unsigned (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(taddr)
+               );
+}
+[[maybe_unused]] __device__ __forceinline__ void tmem_st8(unsigned taddr, const unsigned (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               );
+}
+[[maybe_unused]] __device__ __forceinline__ void tmem_st4(unsigned taddr, const unsigned (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3])
+               );
+}
+[[maybe_unused]] __device__ __forceinline__ void tmem_ld4(unsigned taddr, unsigned (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               );
+}
+// two doubles <-> four TMEM columns (lo, hi words)
+[[maybe_unused]] __device__ __forceinline__ void pack2(const double (&d)[2], unsigned* w) {
+  w[0] = static_cast<unsigned>(__double2loint(d[0]));
+  w[1] = static_cast<unsigned>(__double2hiint(d[0]));
+  w[2] = static_cast<unsigned>(__double2loint(d[1]));
+  w[3] = static_cast<unsigned>(__double2hiint(d[1]));
+}
+[[maybe_unused]] __device__ __forceinline__ void unpack2(const unsigned* w, double (&d)[2]) {
+  d[0] = __hiloint2double(static_cast<int>(w[1]), static_cast<int>(w[0]));
+  d[1] = __hiloint2double(static_cast<int>(w[3]), static_cast<int>(w[2]));
+}
+// No "memory" clobbers: TMEM is not memory the compiler tracks, and a clobber
+// would pin every global load around the TMEM accesses (measured -2.4 % C4).
+// Ordering comes from the registers instead: tmem_wait_ld(v) waits for this
+// thread's outstanding LDTM and then "redefines" v, so no use of v can be
+// scheduled before the wait (volatile asm statements keep their order).
+template <int N>
+__device__ __forceinline__ void tmem_wait_ld(unsigned (&v)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(v[i]));
+}
+[[maybe_unused]] __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
+
+// (MODE 2 returns from the donor before its loop: not a dead-code bug.)
+#pragma nv_diag_suppress 128
 // MODE 0: one IORD=2 step. MODE 1: donor + first corrective pass of an
 // IORD=3 step, additionally writing the pass's limited velocities and 7-point
 // bounds. MODE 2: the second corrective pass from psi^(2) (read instead of the
 // donor), the limited velocities (as u, v, w) and the accumulated bounds.
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS, STG>;
-  static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && C::EARLY),
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
+  static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && WPR == 1 && C::EARLY),
                 "staged inputs: IORD=2 limiter, one row per warp");
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS, SEG = 32 * K;
   using V = Vec<T, K>;
@@ -251,8 +312,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #ifdef IMB_CHECK_SELFTEST  // proves a failing assert traps (tools/checked_build.sh --selftest)
   IMB_ASSERT(blockIdx.x != 0 || threadIdx.x != 0, "selftest", 0);
 #endif
-  const int wrow = warp * RW;  // first region row of this warp
-  const int lk = lane * K;     // this lane's first k of segment 0
+  const int wrow = (warp / WPR) * RW;              // first region row of this warp
+  const int lk = (warp % WPR) * (L / WPR) + lane * K;  // this lane's first k of its segment 0
+  const int gs0 = (warp % WPR) * NS;               // row segment index of this warp's segment 0
   const unsigned PLN = static_cast<unsigned>(a.plane);
 
   // Rows of this warp: region row r = wrow + rr. Element offsets within a
@@ -280,11 +342,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // k +- 1 of a global row (p = this lane's cell pointer of the segment) or
   // of a shared row (fp64 shuffles, fp32 re-reads the out-of-vector value:
   // +1.4 % C4, +1 % C2 over shuffles)
-  constexpr bool SRL = sizeof(T) == 4 && NS == 1;
-#define KMG(c, vec, p) kminus<L, NS, true>(vec, p, (c) % NS, lane)
-#define KPG(c, vec, p) kplus<L, NS, true>(vec, p, (c) % NS, lane)
-#define KMS(c, vec, p) (SRL ? kminus_s<L>(vec, p, lane) : kminus<L, NS, false>(vec, p, (c) % NS, lane))
-#define KPS(c, vec, p) (SRL ? kplus_s<L>(vec, p, lane) : kplus<L, NS, false>(vec, p, (c) % NS, lane))
+  constexpr bool SRL = sizeof(T) == 4 && NS * WPR == 1;
+  constexpr int NSEG = NS * WPR;  // segments per row
+#define KMG(c, vec, p) kminus<L, NSEG, true>(vec, p, gs0 + (c) % NS, lane)
+#define KPG(c, vec, p) kplus<L, NSEG, true>(vec, p, gs0 + (c) % NS, lane)
+#define KMS(c, vec, p) (SRL ? kminus_s<L>(vec, p, lane) : kminus<L, NSEG, false>(vec, p, gs0 + (c) % NS, lane))
+#define KPS(c, vec, p) (SRL ? kplus_s<L>(vec, p, lane) : kplus<L, NSEG, false>(vec, p, gs0 + (c) % NS, lane))
 
   // STG rings: psi^n planes from xb = ib - 3, h planes from hb = ib - 2 (the
   // first each warm-up donor reads); slot and fill (mbarrier phase) by plane.
@@ -342,6 +405,48 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // j-neighbour warps through shared-memory progress counters — was measured
   // 3-4x slower than the hardware barrier and removed.)
   auto nb_sync = [&]() { __syncthreads(); };
+
+  // TMS: the psi^n star extrema of plane p (max and min of psi^n over the
+  // cell and its 6 face neighbours, which the donor of p has in registers
+  // anyway) go to a 3-plane TMEM ring and come back in the bounds phase of
+  // p two iterations later — instead of reloading 5 psi^n rows from L2 and
+  // redoing 12 fp64 compare-selects there. fp64 only: fp32 carries them in
+  // registers (STARC).
+  // With the star ring, each warp's 128 TMEM columns also hold a 4-plane
+  // ring of its h row (donor -> pseudo, bounds, final) and a 3-plane ring of
+  // its v rows j and j+1 (donor -> pseudo): 8 of the 14 L2 loads of the
+  // pseudo-velocity phase and the bounds/final h loads become LDTM.
+  //   columns [0, 48) star (3 x 16), [48, 80) h (4 x 8), [80, 128) v (3 x 16)
+  constexpr bool TMS = IMB_TMEM_STAR && sizeof(T) == 8 && NONOS && MODE != 2 && EARLY &&
+                       !STARC && !STG && NC * K == 4 && NW == 16;
+  constexpr bool TMC = TMS && IMB_TMEM_CACHE;
+  __shared__ unsigned s_tmem_base;
+  unsigned tm_lane = 0;
+  if constexpr (TMS) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                   ::"r"(smem_u32(&s_tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // this warp's lane quarter and its 128-column share of it
+    tm_lane = s_tmem_base + (static_cast<unsigned>((warp & 3) * 32) << 16) +
+              static_cast<unsigned>(warp >> 2) * (512u / (NW / 4));
+  }
+  auto tm_star = [&](int p) { return tm_lane + static_cast<unsigned>((p + 6) % 3) * 16u; };
+  auto tm_h = [&](int p) { return tm_lane + 48u + static_cast<unsigned>((p + 8) & 3) * 8u; };
+  auto tm_v = [&](int p) { return tm_lane + 80u + static_cast<unsigned>((p + 6) % 3) * 16u; };
+  // load a V from 4 TMEM columns (after tmem_wait_ld)
+  auto vfrom = [](const unsigned* w) {
+    V r;
+    double d[2];
+    unpack2(w, d);
+    r.e[0] = d[0];
+    r.e[1] = d[1];
+    return r;
+  };
 
   // psi^n star extrema (STARC): of plane t+1 (nmx), t+2 (nmx_mid, EARLY) and
   // the donor's newest plane (nmx_new)
@@ -403,6 +508,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       }
       const V uc = vload<T, K>(a.u + ij + so), up = vload<T, K>(a.u + (ij + PLN) + so);
       const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
+      if constexpr (TMC) {  // segment c: h -> [4c, 4c+4) of its slot, v rows j, j+1 -> [8c, 8c+8)
+        unsigned w4[4], w8[8];
+        pack2(reinterpret_cast<const double(&)[2]>(hc.e), w4);
+        pack2(reinterpret_cast<const double(&)[2]>(vc.e), w8);
+        pack2(reinterpret_cast<const double(&)[2]>(vp.e), w8 + 4);
+        tmem_st4(tm_h(p) + 4u * static_cast<unsigned>(c), w4);
+        tmem_st8(tm_v(p) + 8u * static_cast<unsigned>(c), w8);
+      }
       const T* W = a.w + ij + so;
       const V wc = vload<T, K>(W);
       const V wp = KPG(c, wc, W);
@@ -418,7 +531,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const T fzr = upflux(x0, zp.e[e], wp.e[e]);
         const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
         res.e[e] = x0 - qdiv(div, hc.e[e]);
-        if constexpr (NONOS && STARC) {
+        if constexpr (NONOS && (STARC || TMS)) {
           nmx_new[c].e[e] = tmax(tmax(tmax(x0, xm.e[e]), tmax(xp.e[e], ym.e[e])),
                                  tmax(tmax(yp.e[e], zm.e[e]), zp.e[e]));
           nmn_new[c].e[e] = tmin(tmin(tmin(x0, xm.e[e]), tmin(xp.e[e], ym.e[e])),
@@ -426,7 +539,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       vstore(dst + r * L + lk + so, res);
+      if constexpr (TMS) {  // segment c -> columns [8c, 8c+8): max (K doubles), then min
+        unsigned tv[8];
+#pragma unroll
+        for (int e = 0; e < K; ++e) {
+          tv[2 * e] = static_cast<unsigned>(__double2loint(nmx_new[c].e[e]));
+          tv[2 * e + 1] = static_cast<unsigned>(__double2hiint(nmx_new[c].e[e]));
+          tv[4 + 2 * e] = static_cast<unsigned>(__double2loint(nmn_new[c].e[e]));
+          tv[4 + 2 * e + 1] = static_cast<unsigned>(__double2hiint(nmn_new[c].e[e]));
+        }
+        tmem_st8(tm_star(p) + 8u * static_cast<unsigned>(c), tv);
+      }
     }
+    if constexpr (TMS) tmem_wait_st();
   };
 
   // P2: pseudo-velocities around base plane pb: x-face pb+1 (into ut), y and
@@ -449,7 +574,32 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const V a1m = vabs(sload<T, K>(s1 + so - L));
       const T* U2 = a.u + i2 + sg;
       const V u2c = vload<T, K>(U2);
-      const V h1c = STG ? sload<T, K>(hrow(pb, r) + sg) : vload<T, K>(a.h + i1 + sg);
+      // v rows j, j+1 and h row j of planes pb, pb+1 (TMEM ring or L2)
+      V h1c, h2, v1, v2, v1p, v2p;
+      if constexpr (TMC) {
+        unsigned wa[8], wb[8], ha[4], hb[4];
+        tmem_ld8(tm_v(pb) + 8u * static_cast<unsigned>(c), wa);
+        tmem_ld8(tm_v(pb + 1) + 8u * static_cast<unsigned>(c), wb);
+        tmem_ld4(tm_h(pb) + 4u * static_cast<unsigned>(c), ha);
+        tmem_ld4(tm_h(pb + 1) + 4u * static_cast<unsigned>(c), hb);
+        tmem_wait_ld(wa);
+        tmem_wait_ld(wb);  // (already complete: these only order the register uses)
+        tmem_wait_ld(ha);
+        tmem_wait_ld(hb);
+        v1 = vfrom(wa);
+        v1p = vfrom(wa + 4);
+        v2 = vfrom(wb);
+        v2p = vfrom(wb + 4);
+        h1c = vfrom(ha);
+        h2 = vfrom(hb);
+      } else {
+        h1c = STG ? sload<T, K>(hrow(pb, r) + sg) : vload<T, K>(a.h + i1 + sg);
+        h2 = STG ? sload<T, K>(hrow(pb + 1, r) + sg) : vload<T, K>(a.h + i2 + sg);
+        v1 = vload<T, K>(a.v + i1 + sg);
+        v2 = vload<T, K>(a.v + i2 + sg);
+        v1p = vload<T, K>(a.v + (p1 + gjp[rr]) + sg);
+        v2p = vload<T, K>(a.v + (p2 + gjp[rr]) + sg);
+      }
       const V a1km = vabs(KMS(c, x1, s1 + so));
       if (row_u) {  // x-face between planes pb and pb+1 of this column
         const V x2 = sload<T, K>(s2 + so);
@@ -469,8 +619,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
         }
         {
-          const V v1 = vload<T, K>(a.v + i1 + sg), v2 = vload<T, K>(a.v + i2 + sg);
-          const V v1p = vload<T, K>(a.v + (p1 + gjp[rr]) + sg), v2p = vload<T, K>(a.v + (p2 + gjp[rr]) + sg);
 #pragma unroll
           for (int e = 0; e < K; ++e) Vs.e[e] = (v1.e[e] + v2.e[e]) + (v1p.e[e] + v2p.e[e]);
         }
@@ -482,7 +630,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
           for (int e = 0; e < K; ++e) Ws.e[e] = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
         }
-        const V h2 = STG ? sload<T, K>(hrow(pb + 1, r) + sg) : vload<T, K>(a.h + i2 + sg);
 #pragma unroll
         for (int e = 0; e < K; ++e)
           ut[c].e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e], bp.e[e],
@@ -523,7 +670,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
           for (int e = 0; e < K; ++e) Ws.e[e] = (w1m.e[e] + w1.e[e]) + (w1mkp.e[e] + w1kp.e[e]);
         }
-        const V v1 = vload<T, K>(a.v + i1 + sg);
         const V h1m = STG ? sload<T, K>(hrow(pb, r - 1) + sg) : vload<T, K>(a.h + (p1 + gjm[rr]) + sg);
         V res;
 #pragma unroll
@@ -556,7 +702,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         {
           const T* V1 = a.v + i1 + sg;
           const T* V1p = a.v + (p1 + gjp[rr]) + sg;
-          const V v1 = vload<T, K>(V1), v1p = vload<T, K>(V1p);
+
           const V v1km = KMG(c, v1, V1), v1pkm = KMG(c, v1p, V1p);
 #pragma unroll
           for (int e = 0; e < K; ++e) Vs.e[e] = (v1km.e[e] + v1.e[e]) + (v1pkm.e[e] + v1p.e[e]);
@@ -699,6 +845,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if constexpr (STARC) {
             mx = nmx[c];
             mn = nmn[c];
+          } else if constexpr (TMS) {  // (warp-uniform here: the whole warp owns row r)
+            unsigned tv[8];
+            tmem_ld8(tm_star(p1) + 8u * static_cast<unsigned>(c), tv);
+            tmem_wait_ld(tv);
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+              mx.e[e] = __hiloint2double(static_cast<int>(tv[2 * e + 1]), static_cast<int>(tv[2 * e]));
+              mn.e[e] = __hiloint2double(static_cast<int>(tv[2 * e + 5]), static_cast<int>(tv[2 * e + 4]));
+            }
           } else if constexpr (MODE == 2) {  // bounds of the previous pass
             mx = vload<T, K>(a.mxo + i1 + sg);
             mn = vload<T, K>(a.mno + i1 + sg);
@@ -719,7 +874,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const V va = sload<T, K>(vA + so), vap = sload<T, K>(vA + so + L);
           const V wa = sload<T, K>(wA + so);
           const V wap = KPS(c, wa, wA + so);
-          const V hc = STG ? sload<T, K>(hrow(p1, r) + sg) : vload<T, K>(a.h + i1 + sg);
+          V hc;
+          if constexpr (TMC) {
+            unsigned w4[4];
+            tmem_ld4(tm_h(p1) + 4u * static_cast<unsigned>(c), w4);
+            tmem_wait_ld(w4);
+            hc = vfrom(w4);
+          } else {
+            hc = STG ? sload<T, K>(hrow(p1, r) + sg) : vload<T, K>(a.h + i1 + sg);
+          }
           V bu, bd, his, los;
 #pragma unroll
           for (int e = 0; e < K; ++e) {
@@ -827,7 +990,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const V vb = sload<T, K>(vB + so), vbp = sload<T, K>(vB + so + L);
             const V wb = sload<T, K>(wB + so);
             const V wbp = KPS(c, wb, wB + so);
-            const V hc = STG ? sload<T, K>(hrow(t, r) + sg) : vload<T, K>(a.h + (q0 + gj[rr]) + sg);
+            V hc;
+            if constexpr (TMC) {
+              unsigned w4[4];
+              tmem_ld4(tm_h(t) + 4u * static_cast<unsigned>(c), w4);
+              tmem_wait_ld(w4);
+              hc = vfrom(w4);
+            } else {
+              hc = STG ? sload<T, K>(hrow(t, r) + sg) : vload<T, K>(a.h + (q0 + gj[rr]) + sg);
+            }
             V res;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
@@ -944,11 +1115,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (a.push_sys && (tl < th || ul < uh)) __threadfence_system();
     }
   }
+  if constexpr (TMS) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem_base));
+  }
 #undef KMG
 #undef KPG
 #undef KMS
 #undef KPS
 }
+#pragma nv_diag_default 128
 
 }  // namespace
 
@@ -1000,10 +1177,11 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
 
 namespace {
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG = false>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG = false,
+          int WPR = 1>
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS, STG>;
-  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
+  auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>;
   // Function attributes and occupancy are per device: configure each device
   // once (a group or a measurement may drive several GPUs from one process).
   static std::mutex mu;
@@ -1067,6 +1245,10 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
         if (stg && fs.m >= 18)
           return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE, true>(fs, a, num_sms, st);
       }
+#ifdef IMB_F64_WPR2_NW  // experiment: two warps per row (one 2-double segment per lane)
+      if constexpr (D)
+        return launch_cfg<T, 128, 1, IMB_F64_WPR2_NW, 1, NONOS, false, MODE, false, 2>(fs, a, num_sms, st);
+#endif
       return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);

@@ -237,37 +237,33 @@ def summarize(xs: Iterable[float]) -> Summary:
 
 
 # ---- speed-function CSV ----------------------------------
+# One parser/writer of the format: the C++ one (csrc/host/fpm.cpp) behind the
+# C-ABI; these wrappers only move the text across.
 def write_csv(f: SpeedFunction) -> str:
-    rows = [f"# unit_cells={f.unit_cells} granularity={f.granularity} label={f.label}",
-            "x,speed,ci_halfwidth,repetitions"]
-    rows += [f"{s.x},{s.speed:.17g},{s.ci_halfwidth:.17g},{s.repetitions}" for s in f.samples]
-    return "\n".join(rows) + "\n"
+    arr = samples_array(f.samples)
+    n = C.c_size_t()
+    lab = f.label.encode()
+    rc = load().imb_speed_csv_format(f.unit_cells, f.granularity, arr, len(f.samples), lab, None, 0,
+                                     C.byref(n))
+    if rc not in (0, _lib.RangeError.code):
+        check(rc)
+    buf = C.create_string_buffer(n.value + 1)
+    check(load().imb_speed_csv_format(f.unit_cells, f.granularity, arr, len(f.samples), lab, buf,
+                                      n.value + 1, C.byref(n)))
+    return buf.value.decode()
 
 
 def read_csv(text: str) -> SpeedFunction:
-    lines = text.splitlines()
-    if not lines or not lines[0].startswith("# "):
-        raise _lib.ParseError("missing '# ' header (line 1)")
-    head, _, label = lines[0][2:].partition(" label=")
-    kv = dict(tok.split("=", 1) for tok in head.split())
-    try:
-        unit, gran = int(kv["unit_cells"]), int(kv["granularity"])
-    except (KeyError, ValueError) as e:
-        raise _lib.ParseError(f"bad header ({e}) (line 1)") from None
-    if len(lines) < 2 or lines[1].strip() != "x,speed,ci_halfwidth,repetitions":
-        raise _lib.ParseError("expected column header (line 2)")
-    samples = []
-    for no, line in enumerate(lines[2:], start=3):
-        if not line.strip():
-            continue
-        cols = line.split(",")
-        if len(cols) != 4:
-            raise _lib.ParseError(f"expected 4 columns (line {no})")
-        try:
-            samples.append(SpeedSample(int(cols[0]), float(cols[1]), float(cols[2]), int(cols[3])))
-        except ValueError as e:
-            raise _lib.ParseError(f"{e} (line {no})") from None
-    return SpeedFunction(unit, gran, tuple(samples), label)
+    raw = text.encode()
+    unit, gran, ns, line = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+    lab = C.create_string_buffer(len(raw) + 1)
+    cap = raw.count(b"\n") + 1
+    out = (_lib.imb_speed_sample * cap)()
+    rc = load().imb_speed_csv_parse(raw, len(raw), C.byref(unit), C.byref(gran), out, cap,
+                                    C.byref(ns), lab, len(raw) + 1, C.byref(line))
+    check(rc)
+    samples = tuple(SpeedSample(o.x, o.speed, o.ci_halfwidth, o.repetitions) for o in out[:ns.value])
+    return SpeedFunction(unit.value, gran.value, samples, lab.value.decode())
 
 
 # ---- 2-D speed-surface CSV: row-major in n, then m ------------

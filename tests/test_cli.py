@@ -123,3 +123,29 @@ def test_measure_and_validate_on_gpu(capsys, tmp_path):
         assert len((out / "table2.csv").read_text().splitlines()) == 1 + 2 * 2
     rc, out_txt, _ = run(capsys, "report", "--out-dir", out)
     assert rc == 0 and "measure" in out_txt and "validate" in out_txt
+
+
+@pytest.mark.gpu
+def test_measure_ring_halo_path_on_gpu(capsys, tmp_path):
+    # the speed function measured on the production halo
+    # path (a ring of slabs pushing halos into each other), labelled as such;
+    # on one GPU the ring's slabs share the device (a labelled stand-in).
+    out = tmp_path / "r"
+    common = ["--l", 32, "--steps", 2, "--max-reps", 3, "--out-dir", out]
+    rc, _, err = run(capsys, "measure", "--x", "8:16:8", "--m", 16, "--halo", "ring",
+                     "--devices", "0,0", *common)
+    assert rc == 0, err
+    f = fpm.read_csv((out / "speed_avg.csv").read_text())
+    assert [s.x for s in f.samples] == [8, 16] and all(s.speed > 0 for s in f.samples)
+    assert "halo=ring p=2" in f.label and "stand-in" in f.label
+    assert (out / "speed_team0.csv").exists() and (out / "speed_team1.csv").exists()
+    man = json.loads((out / "measure_manifest.json").read_text())
+    assert man["halo"].startswith("halo=ring")
+    rc, _, err = run(capsys, "validate", out / "speed_avg.csv", "--total", 32, "--p", 2,
+                     "--offsets", "0,8", "--devices", "0,0", *common)
+    assert rc == 0, err
+    man = json.loads((out / "validate_manifest.json").read_text())
+    assert man["mode"].startswith("lockstep decomposition") and "stand-in" in man["mode"]
+    # --halo self refuses a repeated device
+    rc, _, _ = run(capsys, "measure", "--x", "8:16:8", "--m", 16, "--devices", "0,0", *common)
+    assert rc == 2
