@@ -344,8 +344,8 @@ def main():
             # per clock (148 SMs, max SM clock); FP pipe floor: the step's
             # FP64 (fp32: FMA) pipe busy cycles, i.e. its measured utilisation
             # times its ncu duration. frac = floor / this run's step time.
-            clk = 1965e6
-            issue_ms = rec["warp_inst_per_step"] / (148 * 4 * clk) * 1e3
+            sm_hz = 1965e6
+            issue_ms = rec["warp_inst_per_step"] / (148 * 4 * sm_hz) * 1e3
             pipe_ms = rec["fp_pipe_active_pct"] / 100.0 * rec["ncu_ms_per_step"]
             compute = {"issue_floor_ms": issue_ms, "issue_frac": issue_ms / (per_step * 1e3),
                        "fp_pipe": rec["fp_pipe"], "fp_pipe_floor_ms": pipe_ms,

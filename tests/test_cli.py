@@ -132,11 +132,12 @@ def test_measure_ring_halo_path_on_gpu(capsys, tmp_path):
     # on one GPU the ring's slabs share the device (a labelled stand-in).
     out = tmp_path / "r"
     common = ["--l", 32, "--steps", 2, "--max-reps", 3, "--out-dir", out]
-    rc, _, err = run(capsys, "measure", "--x", "8:16:8", "--m", 16, "--halo", "ring",
+    rc, _, err = run(capsys, "measure", "--x", "8:24:8", "--m", 16, "--halo", "ring",
                      "--devices", "0,0", *common)
     assert rc == 0, err
     f = fpm.read_csv((out / "speed_avg.csv").read_text())
-    assert [s.x for s in f.samples] == [8, 16] and all(s.speed > 0 for s in f.samples)
+    # validate's offset 8 around 32/2 = 16 needs shares 8 and 24 inside the model
+    assert [s.x for s in f.samples] == [8, 16, 24] and all(s.speed > 0 for s in f.samples)
     assert "halo=ring p=2" in f.label and "stand-in" in f.label
     assert (out / "speed_team0.csv").exists() and (out / "speed_team1.csv").exists()
     man = json.loads((out / "measure_manifest.json").read_text())
