@@ -76,7 +76,8 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_TWO_F64 0
 #endif
 
-template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false, int WPR = 1>
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false, int WPR = 1,
+          bool TMWB = false>
 struct Cfg {
   // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
   static constexpr int KPT = L / (32 * NS * WPR);  // consecutive k per lane and segment
@@ -98,7 +99,12 @@ struct Cfg {
   // plane's pseudo-velocities off the ones a slower warp's final update reads.
   static constexpr bool TWO = EARLY && (sizeof(T) == 4 ? IMB_TWO_F32 : IMB_TWO_F64);
   static constexpr int NVW = NONOS ? (TWO ? 3 : 2) : 1;  // y- and z-velocity slots each
-  static constexpr int NSLOT = NONOS ? NX1 + 2 * NVW + 4 : 5;
+  // TMWB: the z-face velocities and the betas' second plane live in tensor
+  // memory (per-thread), so shared memory keeps no z-velocity slot and one
+  // beta slot each (see k_fused)
+  static constexpr int NWS = TMWB ? 0 : NVW;             // z-velocity slots
+  static constexpr int NBS = TMWB ? 1 : 2;               // beta slots (up and down each)
+  static constexpr int NSLOT = NONOS ? NX1 + NVW + NWS + 2 * NBS : 5;
   // STG: psi^n and h staged in shared memory by bulk async copies (TMA engine)
   // into rings of 4 (psi^n, rows -1..RR) and 5 (h, rows 0..RR-1) planes, each
   // slot with its own mbarrier.
@@ -213,9 +219,27 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_TMEM_STAR  // psi^n star extrema carried in tensor memory (fp64, see k_fused)
 #define IMB_TMEM_STAR 1
 #endif
-#ifndef IMB_TMEM_CACHE  // h and v rows cached in tensor memory across iterations (fp64)
+#ifndef IMB_TMEM_CACHE  // h (and v, without IMB_TMEM_WB) rows cached in tensor memory (fp64)
 #define IMB_TMEM_CACHE 1
 #endif
+#ifndef IMB_TMEM_WB  // z-face velocities and the older beta plane in tensor memory (fp64)
+#define IMB_TMEM_WB 1
+#endif
+
+// Instantiations that use tensor memory as per-thread storage (fp64 IORD=2
+// limiter shapes with one 4-double lane vector per row): TMS (psi^n star
+// ring + caches) and TMWB (z-face velocities and betas, see k_fused).
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
+constexpr bool use_tms() {
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
+  return IMB_TMEM_STAR && sizeof(T) == 8 && NONOS && MODE != 2 && C::EARLY && !STARC && !STG &&
+         RW * NS * C::KPT == 4 && NW == 16;
+}
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
+constexpr bool use_tmwb() {
+  return use_tms<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>() && IMB_TMEM_WB && IMB_TMEM_CACHE &&
+         !Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>::TWO;
+}
 
 // ---- tensor memory (TMEM) as per-thread storage ------------------------------
 // The stencil has no MMA, so the SM's 256 KB of TMEM is free: a warp reads
@@ -277,7 +301,8 @@ __device__ __forceinline__ void tmem_wait_ld(unsigned (&v)[N]) {
 // donor), the limited velocities (as u, v, w) and the accumulated bounds.
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
+  constexpr bool TMWB = use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB>;
   static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && WPR == 1 && C::EARLY),
                 "staged inputs: IORD=2 limiter, one row per warp");
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS, SEG = 32 * K;
@@ -287,11 +312,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   T* s_x1 = sm;                          // psi^(1) slots, by plane
   constexpr bool EARLY = C::EARLY;
   T* s_v = sm + C::NX1 * PL;             // y-face pseudo-velocities
-  T* s_w = s_v + C::NVW * PL;            // z-face pseudo-velocities
-  T* s_bu = s_w + C::NVW * PL;           // beta up,   2 slots (NONOS)
+  T* s_w = s_v + C::NVW * PL;            // z-face pseudo-velocities (not with TMWB)
+  T* s_bu = s_w + C::NWS * PL;           // beta up,   NBS slots (NONOS)
   constexpr bool TWO = C::TWO;
   auto vws = [](int p) { return C::NVW == 3 ? (p + 6) % 3 : (p & 1); };  // p >= -3
-  T* s_bd = s_bu + 2 * PL;               // beta down, 2 slots (NONOS)
+  T* s_bd = s_bu + C::NBS * PL;          // beta down, NBS slots (NONOS)
   T* s_xs = s_x1 + C::NSLOT * PL;                 // STG: psi^n ring
   T* s_hs = s_xs + C::NXS * C::XROWS * L;         // STG: h ring
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(s_hs + C::NHS * C::HROWS * L);
@@ -417,9 +442,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // its v rows j and j+1 (donor -> pseudo): 8 of the 14 L2 loads of the
   // pseudo-velocity phase and the bounds/final h loads become LDTM.
   //   columns [0, 48) star (3 x 16), [48, 80) h (4 x 8), [80, 128) v (3 x 16)
-  constexpr bool TMS = IMB_TMEM_STAR && sizeof(T) == 8 && NONOS && MODE != 2 && EARLY &&
-                       !STARC && !STG && NC * K == 4 && NW == 16;
-  constexpr bool TMC = TMS && IMB_TMEM_CACHE;
+  //
+  // TMWB (instead of the v rows): the z-face pseudo-velocities and the betas
+  // are only ever read by the thread that computed them (the k +- 1 partner
+  // is a shuffle away), apart from beta's j-1 read of the newest plane. So
+  // the z-velocities of planes t and t+1 and this thread's betas of the older
+  // plane go to TMEM, and shared memory keeps one beta plane (up, down) and no
+  // z-velocity plane: 64 KB less shared memory, i.e. 64 KB more L1.
+  //   columns [80, 112) betas (2 planes x 16: segment c -> up [8c, 8c+4), down [8c+4, 8c+8)),
+  //           [112, 128) z-velocities (2 planes x 8: segment c -> [4c, 4c+4))
+  constexpr bool TMS = use_tms<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
+  constexpr bool TMH = TMS && IMB_TMEM_CACHE;   // h ring
+  constexpr bool TMC = TMH && !TMWB;            // v rows ring
   __shared__ unsigned s_tmem_base;
   unsigned tm_lane = 0;
   if constexpr (TMS) {
@@ -438,6 +472,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   auto tm_star = [&](int p) { return tm_lane + static_cast<unsigned>((p + 6) % 3) * 16u; };
   auto tm_h = [&](int p) { return tm_lane + 48u + static_cast<unsigned>((p + 8) & 3) * 8u; };
   auto tm_v = [&](int p) { return tm_lane + 80u + static_cast<unsigned>((p + 6) % 3) * 16u; };
+  auto tm_b = [&](int p) { return tm_lane + 80u + static_cast<unsigned>(p & 1) * 16u; };
+  auto tm_w = [&](int p) { return tm_lane + 112u + static_cast<unsigned>(p & 1) * 8u; };
   // load a V from 4 TMEM columns (after tmem_wait_ld)
   auto vfrom = [](const unsigned* w) {
     V r;
@@ -446,6 +482,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     r.e[0] = d[0];
     r.e[1] = d[1];
     return r;
+  };
+  // TMWB: z-velocities of plane p, segment c, and their k+1 neighbours. The
+  // two segments of a row are one TMEM load; lane 31's neighbour is lane 0's
+  // first cell of the next segment (of segment 0 after the last: periodic),
+  // which lane 0 offers in place of its own to the single shuffle.
+  auto tm_wk = [&](int p, int c, V& wc, V& wcp) {
+    static_assert(!TMWB || (NC == 2 && K == 2), "TMWB is written for 2 segments of 2 doubles");
+    unsigned t8[8];
+    tmem_ld8(tm_w(p), t8);
+    tmem_wait_ld(t8);
+    const V s0 = vfrom(t8), s1 = vfrom(t8 + 4);
+    wc = c == 0 ? s0 : s1;
+    const T offer = lane == 0 ? (c == 0 ? s1.e[0] : s0.e[0]) : wc.e[0];
+    wcp.e[0] = wc.e[1];
+    wcp.e[1] = __shfl_sync(kFull, offer, (lane + 1) & 31);
   };
 
   // psi^n star extrema (STARC): of plane t+1 (nmx), t+2 (nmx_mid, EARLY) and
@@ -508,12 +559,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       }
       const V uc = vload<T, K>(a.u + ij + so), up = vload<T, K>(a.u + (ij + PLN) + so);
       const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
-      if constexpr (TMC) {  // segment c: h -> [4c, 4c+4) of its slot, v rows j, j+1 -> [8c, 8c+8)
-        unsigned w4[4], w8[8];
+      if constexpr (TMH) {  // segment c: h -> [4c, 4c+4) of its slot
+        unsigned w4[4];
         pack2(reinterpret_cast<const double(&)[2]>(hc.e), w4);
+        tmem_st4(tm_h(p) + 4u * static_cast<unsigned>(c), w4);
+      }
+      if constexpr (TMC) {  // v rows j, j+1 -> [8c, 8c+8)
+        unsigned w8[8];
         pack2(reinterpret_cast<const double(&)[2]>(vc.e), w8);
         pack2(reinterpret_cast<const double(&)[2]>(vp.e), w8 + 4);
-        tmem_st4(tm_h(p) + 4u * static_cast<unsigned>(c), w4);
         tmem_st8(tm_v(p) + 8u * static_cast<unsigned>(c), w8);
       }
       const T* W = a.w + ij + so;
@@ -576,7 +630,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const V u2c = vload<T, K>(U2);
       // v rows j, j+1 and h row j of planes pb, pb+1 (TMEM ring or L2)
       V h1c, h2, v1, v2, v1p, v2p;
-      if constexpr (TMC) {
+      if constexpr (TMH && !TMC) {
+        unsigned ha[4], hb[4];
+        tmem_ld4(tm_h(pb) + 4u * static_cast<unsigned>(c), ha);
+        tmem_ld4(tm_h(pb + 1) + 4u * static_cast<unsigned>(c), hb);
+        v1 = vload<T, K>(a.v + i1 + sg);
+        v2 = vload<T, K>(a.v + i2 + sg);
+        v1p = vload<T, K>(a.v + (p1 + gjp[rr]) + sg);
+        v2p = vload<T, K>(a.v + (p2 + gjp[rr]) + sg);
+        tmem_wait_ld(ha);
+        tmem_wait_ld(hb);
+        h1c = vfrom(ha);
+        h2 = vfrom(hb);
+      } else if constexpr (TMC) {
         unsigned wa[8], wb[8], ha[4], hb[4];
         tmem_ld8(tm_v(pb) + 8u * static_cast<unsigned>(c), wa);
         tmem_ld8(tm_v(pb + 1) + 8u * static_cast<unsigned>(c), wb);
@@ -713,8 +779,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         for (int e = 0; e < K; ++e)
           res.e[e] = pseudo_face<T>(w1.e[e], h1km.e[e], h1c.e[e], a1.e[e], a1km.e[e], bp.e[e],
                                     bm.e[e], Us.e[e], cp.e[e], cm.e[e], Vs.e[e]);
-        vstore(wdst + so, res);
+        if constexpr (TMWB) {
+          unsigned w4[4];
+          pack2(reinterpret_cast<const double(&)[2]>(res.e), w4);
+          tmem_st4(tm_w(pb) + 4u * static_cast<unsigned>(c), w4);
+        } else {
+          vstore(wdst + so, res);
+        }
       }
+    }
+    if constexpr (TMWB) {
+      if (!only_u) tmem_wait_st();
     }
   };
 
@@ -811,8 +886,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       T* wA = s_w + vws(p1) * PL;
       const T* vB = s_v + vws(t) * PL;         // limited, plane t
       const T* wB = s_w + vws(t) * PL;
-      T* buA = s_bu + (p1 & 1) * PL;            // beta, plane t+1
-      T* bdA = s_bd + (p1 & 1) * PL;
+      T* buA = s_bu + (C::NBS == 2 ? (p1 & 1) : 0) * PL;  // beta, plane t+1
+      T* bdA = s_bd + (C::NBS == 2 ? (p1 & 1) : 0) * PL;
       const T* buB = s_bu + ((p1 + 1) & 1) * PL;  // beta, plane t
       const T* bdB = s_bd + ((p1 + 1) & 1) * PL;
       stage_pseudo(p1, false, ufresh, vA, wA);
@@ -872,8 +947,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             }
           }
           const V va = sload<T, K>(vA + so), vap = sload<T, K>(vA + so + L);
-          const V wa = sload<T, K>(wA + so);
-          const V wap = KPS(c, wa, wA + so);
+          V wa, wap;
+          if constexpr (TMWB) {
+            tm_wk(p1, c, wa, wap);
+          } else {
+            wa = sload<T, K>(wA + so);
+            wap = KPS(c, wa, wA + so);
+          }
           V hc;
           if constexpr (TMC) {
             unsigned w4[4];
@@ -919,6 +999,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
           vstore(buA + so, bu);
           vstore(bdA + so, bd);
+          if constexpr (TMWB) {  // this thread's betas of plane t+1, for its own x-face limit next iteration
+            unsigned t8[8];
+            pack2(reinterpret_cast<const double(&)[2]>(bu.e), t8);
+            pack2(reinterpret_cast<const double(&)[2]>(bd.e), t8 + 4);
+            tmem_st8(tm_b(p1) + 8u * static_cast<unsigned>(c), t8);
+          }
           if constexpr (MODE == 1) {  // bounds for the next pass
             if (keep(t, r)) {
               vstore(a.mxo + i1 + sg, his);
@@ -930,6 +1016,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if constexpr (TWO) {
         if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
       }
+      if constexpr (TMWB) tmem_wait_st();
       IMB_T(5)
       nb_sync();
       IMB_T(6)
@@ -962,9 +1049,22 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if (r >= RR - 2) continue;
           V fxr;
           {
-            const V wa = sload<T, K>(wA + so);
+            V wa, buo, bdo;
+            if constexpr (TMWB) {
+              unsigned t8[8], w4[4];
+              tmem_ld8(tm_b(t) + 8u * static_cast<unsigned>(c), t8);
+              tmem_ld4(tm_w(p1) + 4u * static_cast<unsigned>(c), w4);
+              tmem_wait_ld(t8);
+              tmem_wait_ld(w4);
+              buo = vfrom(t8);
+              bdo = vfrom(t8 + 4);
+              wa = vfrom(w4);
+            } else {
+              wa = sload<T, K>(wA + so);
+              buo = sload<T, K>(buB + so);
+              bdo = sload<T, K>(bdB + so);
+            }
             const V bukm = KMS(c, bu, buA + so), bdkm = KMS(c, bd, bdA + so);
-            const V buo = sload<T, K>(buB + so), bdo = sload<T, K>(bdB + so);
             const V xc = sload<T, K>(s0 + so);
             const V x1 = sload<T, K>(s1 + so);
             V wres, uls;
@@ -975,7 +1075,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               uls.e[e] = ul;
               fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
             }
-            vstore(wA + so, wres);
+            if constexpr (TMWB) {
+              unsigned w4[4];
+              pack2(reinterpret_cast<const double(&)[2]>(wres.e), w4);
+              tmem_st4(tm_w(p1) + 4u * static_cast<unsigned>(c), w4);
+            } else {
+              vstore(wA + so, wres);
+            }
             if constexpr (MODE == 1) {
               if (keep(t, r)) {
                 vstore(a.wo + (q1 + gj[rr]) + sg, wres);
@@ -988,8 +1094,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
             const V zm = KMS(c, xc, s0 + so), zp = KPS(c, xc, s0 + so);
             const V vb = sload<T, K>(vB + so), vbp = sload<T, K>(vB + so + L);
-            const V wb = sload<T, K>(wB + so);
-            const V wbp = KPS(c, wb, wB + so);
+            V wb, wbp;
+            if constexpr (TMWB) {
+              tm_wk(t, c, wb, wbp);
+            } else {
+              wb = sload<T, K>(wB + so);
+              wbp = KPS(c, wb, wB + so);
+            }
             V hc;
             if constexpr (TMC) {
               unsigned w4[4];
@@ -1016,6 +1127,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           fxc[c] = fxr;
         }
       }
+      if constexpr (TMWB) tmem_wait_st();
       IMB_T(9)
       if constexpr (EARLY && !TWO) {
         if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
@@ -1180,7 +1292,8 @@ namespace {
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG = false,
           int WPR = 1>
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
-  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR,
+                use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>()>;
   auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>;
   // Function attributes and occupancy are per device: configure each device
   // once (a group or a measurement may drive several GPUs from one process).
