@@ -226,19 +226,18 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #define IMB_TMEM_WB 1
 #endif
 
-// Instantiations that use tensor memory as per-thread storage (fp64 IORD=2
-// limiter shapes with one 4-double lane vector per row): TMS (psi^n star
-// ring + caches) and TMWB (z-face velocities and betas, see k_fused).
+// Instantiations that use tensor memory as per-thread storage: the fp64
+// limiter shapes with one 4-double lane vector per row (see k_fused: the
+// psi^n star ring, the h and v row rings, and TMWB, the z-face velocities and
+// betas).
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
-constexpr bool use_tms() {
+constexpr bool use_tmem() {
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
-  return IMB_TMEM_STAR && sizeof(T) == 8 && NONOS && MODE != 2 && C::EARLY && !STARC && !STG &&
-         RW * NS * C::KPT == 4 && NW == 16;
+  return sizeof(T) == 8 && NONOS && C::EARLY && !STARC && !STG && RW * NS * C::KPT == 4 && NW == 16;
 }
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
 constexpr bool use_tmwb() {
-  return use_tms<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>() && IMB_TMEM_WB && IMB_TMEM_CACHE &&
-         !Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>::TWO;
+  return use_tmem<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>() && IMB_TMEM_WB && IMB_TMEM_CACHE;
 }
 
 // ---- tensor memory (TMEM) as per-thread storage ------------------------------
@@ -451,12 +450,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // z-velocity plane: 64 KB less shared memory, i.e. 64 KB more L1.
   //   columns [80, 112) betas (2 planes x 16: segment c -> up [8c, 8c+4), down [8c+4, 8c+8)),
   //           [112, 128) z-velocities (2 planes x 8: segment c -> [4c, 4c+4))
-  constexpr bool TMS = use_tms<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
-  constexpr bool TMH = TMS && IMB_TMEM_CACHE;   // h ring
-  constexpr bool TMC = TMH && !TMWB;            // v rows ring
+  //
+  // MODE 2 (pass 3 of IORD=3) reads its bounds instead of a psi^n star, so
+  // its v ring takes the star's columns [0, 48) and it keeps TMWB.
+  constexpr bool TMM = use_tmem<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
+  constexpr bool TMS = TMM && IMB_TMEM_STAR && MODE != 2;     // psi^n star ring
+  constexpr bool TMH = TMM && IMB_TMEM_CACHE;                  // h ring
+  constexpr bool TMC = TMH && (!TMWB || MODE == 2);            // v rows ring
   __shared__ unsigned s_tmem_base;
   unsigned tm_lane = 0;
-  if constexpr (TMS) {
+  if constexpr (TMM) {
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
                    ::"r"(smem_u32(&s_tmem_base)));
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   }
   auto tm_star = [&](int p) { return tm_lane + static_cast<unsigned>((p + 6) % 3) * 16u; };
   auto tm_h = [&](int p) { return tm_lane + 48u + static_cast<unsigned>((p + 8) & 3) * 8u; };
-  auto tm_v = [&](int p) { return tm_lane + 80u + static_cast<unsigned>((p + 6) % 3) * 16u; };
+  auto tm_v = [&](int p) { return tm_lane + (MODE == 2 ? 0u : 80u) + static_cast<unsigned>((p + 6) % 3) * 16u; };
   auto tm_b = [&](int p) { return tm_lane + 80u + static_cast<unsigned>(p & 1) * 16u; };
   auto tm_w = [&](int p) { return tm_lane + 112u + static_cast<unsigned>(p & 1) * 8u; };
   // load a V from 4 TMEM columns (after tmem_wait_ld)
@@ -517,7 +520,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           nmx_new[c] = vload<T, K>(a.mxo + ij + so);
           nmn_new[c] = vload<T, K>(a.mno + ij + so);
         }
+        if constexpr (TMH) {  // the h and v rings, as the donor of MODE 0/1 fills them
+          unsigned w4[4];
+          const V hc = vload<T, K>(a.h + ij + so);
+          pack2(reinterpret_cast<const double(&)[2]>(hc.e), w4);
+          tmem_st4(tm_h(p) + 4u * static_cast<unsigned>(c), w4);
+        }
+        if constexpr (TMC) {
+          unsigned w8[8];
+          const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
+          pack2(reinterpret_cast<const double(&)[2]>(vc.e), w8);
+          pack2(reinterpret_cast<const double(&)[2]>(vp.e), w8 + 4);
+          tmem_st8(tm_v(p) + 8u * static_cast<unsigned>(c), w8);
+        }
       }
+      if constexpr (TMH) tmem_wait_st();
       return;
     }
     if constexpr (STG) {
@@ -955,7 +972,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             wap = KPS(c, wa, wA + so);
           }
           V hc;
-          if constexpr (TMC) {
+          if constexpr (TMH) {
             unsigned w4[4];
             tmem_ld4(tm_h(p1) + 4u * static_cast<unsigned>(c), w4);
             tmem_wait_ld(w4);
@@ -1102,7 +1119,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               wbp = KPS(c, wb, wB + so);
             }
             V hc;
-            if constexpr (TMC) {
+            if constexpr (TMH) {
               unsigned w4[4];
               tmem_ld4(tm_h(t) + 4u * static_cast<unsigned>(c), w4);
               tmem_wait_ld(w4);
@@ -1227,7 +1244,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (a.push_sys && (tl < th || ul < uh)) __threadfence_system();
     }
   }
-  if constexpr (TMS) {
+  if constexpr (TMM) {
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem_base));
