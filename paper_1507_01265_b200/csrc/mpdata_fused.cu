@@ -69,6 +69,9 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_ACC(slot, a, b)
 #endif
 
+#ifndef IMB_F64_NS  // fp64 at l = 128: two segments of 2 doubles per lane (1: one of 4 spills 364 B)
+#define IMB_F64_NS 2
+#endif
 #ifndef IMB_TWO_F32  // two barriers per plane (see Cfg::TWO): fp32 +7.6 % C4, +4 % C5
 #define IMB_TWO_F32 1
 #endif
@@ -150,6 +153,20 @@ struct Args {
   int push_sys;  // push targets may be on a peer GPU (system-scope fence)
 };
 
+// One double loaded by the lanes with `on` only (the seam lane), into a fresh
+// register that the caller selects against the shuffle result.
+template <bool GLOBAL>
+__device__ __forceinline__ double seam_load(const double* q, bool on) {
+  double v;
+  if constexpr (GLOBAL)
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q ld.global.nc.f64 %0, [%2];\n\t}"
+        : "=d"(v) : "r"(static_cast<unsigned>(on)), "l"(q));
+  else
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
+        : "=d"(v) : "r"(static_cast<unsigned>(on)), "r"(static_cast<unsigned>(__cvta_generic_to_shared(q))));
+  return v;
+}
+
 // ---- k +- 1 neighbours of a lane's segment vector ---------------------------
 // A warp holds NS segments of 32*K consecutive k of a row; inside a segment
 // the neighbour is one shuffle away, and with NS == 1 the shuffle also
@@ -165,12 +182,7 @@ __device__ __forceinline__ Vec<T, K> kminus(const Vec<T, K>& a, const T* p, int 
   if constexpr (NS > 1) {
     static_assert(sizeof(T) == 8, "seam reloads are written for fp64");
     const T* q = p + (sg == 0 ? L - 1 : -1);  // lane 0's neighbour (sg is unrolled: an immediate)
-    if constexpr (GLOBAL)
-      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 0;\n\t@q ld.global.nc.f64 %0, [%2];\n\t}"
-          : "+d"(r.e[0]) : "r"(lane), "l"(q));
-    else
-      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 0;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
-          : "+d"(r.e[0]) : "r"(lane), "r"(static_cast<unsigned>(__cvta_generic_to_shared(q))));
+    r.e[0] = lane == 0 ? seam_load<GLOBAL>(q, lane == 0) : r.e[0];
   }
 #pragma unroll
   for (int e = 1; e < K; ++e) r.e[e] = a.e[e - 1];
@@ -185,12 +197,7 @@ __device__ __forceinline__ Vec<T, K> kplus(const Vec<T, K>& a, const T* p, int s
     // p is this lane's first cell of the segment; lane 31 needs the cell
     // after the segment (the next segment's first, or k = 0 after the last)
     const T* q = p + (sg == NS - 1 ? K - L : K);
-    if constexpr (GLOBAL)
-      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 31;\n\t@q ld.global.nc.f64 %0, [%2];\n\t}"
-          : "+d"(r.e[K - 1]) : "r"(lane), "l"(q));
-    else
-      asm("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %1, 31;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
-          : "+d"(r.e[K - 1]) : "r"(lane), "r"(static_cast<unsigned>(__cvta_generic_to_shared(q))));
+    r.e[K - 1] = lane == 31 ? seam_load<GLOBAL>(q, lane == 31) : r.e[K - 1];
   }
 #pragma unroll
   for (int e = 0; e + 1 < K; ++e) r.e[e] = a.e[e + 1];
@@ -224,6 +231,9 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #endif
 #ifndef IMB_TMEM_WB  // z-face velocities and the older beta plane in tensor memory (fp64)
 #define IMB_TMEM_WB 1
+#endif
+#ifndef IMB_TMEM_CARRY  // x-face velocity and x-flux carries in tensor memory (fp64)
+#define IMB_TMEM_CARRY 1
 #endif
 
 // Instantiations that use tensor memory as per-thread storage: the fp64
@@ -267,6 +277,61 @@ constexpr bool use_tmwb() {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(taddr)
                );
+}
+[[maybe_unused]] __device__ __forceinline__ void tmem_ld16(unsigned taddr, unsigned (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(taddr));
+}
+[[maybe_unused]] __device__ __forceinline__ void tmem_st16(unsigned taddr, const unsigned (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld(unsigned taddr, unsigned (&v)[N]) {
+  if constexpr (N == 4) tmem_ld4(taddr, v);
+  else if constexpr (N == 8) tmem_ld8(taddr, v);
+  else if constexpr (N == 16) tmem_ld16(taddr, v);
+  else __trap();  // (instantiated by shapes that never use TMEM)
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(unsigned taddr, const unsigned (&v)[N]) {
+  if constexpr (N == 4) tmem_st4(taddr, v);
+  else if constexpr (N == 8) tmem_st8(taddr, v);
+  else if constexpr (N == 16) tmem_st16(taddr, v);
+  else __trap();  // (instantiated by shapes that never use TMEM)
+}
+// K doubles <-> 2K TMEM columns (lo, hi words); fp32 never stores in TMEM
+template <class T, int K>
+__device__ __forceinline__ void packv(const Vec<T, K>& a, unsigned* w) {
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    if constexpr (sizeof(T) == 8) {
+      w[2 * e] = static_cast<unsigned>(__double2loint(a.e[e]));
+      w[2 * e + 1] = static_cast<unsigned>(__double2hiint(a.e[e]));
+    } else {
+      w[2 * e] = w[2 * e + 1] = __float_as_uint(a.e[e]);
+    }
+  }
+}
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> unpackv(const unsigned* w) {
+  Vec<T, K> r;
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    if constexpr (sizeof(T) == 8)
+      r.e[e] = __hiloint2double(static_cast<int>(w[2 * e + 1]), static_cast<int>(w[2 * e]));
+    else
+      r.e[e] = __uint_as_float(w[2 * e]);
+  }
+  return r;
 }
 // two doubles <-> four TMEM columns (lo, hi words)
 [[maybe_unused]] __device__ __forceinline__ void pack2(const double (&d)[2], unsigned* w) {
@@ -339,6 +404,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   const int wrow = (warp / WPR) * RW;              // first region row of this warp
   const int lk = (warp % WPR) * (L / WPR) + lane * K;  // this lane's first k of its segment 0
   const int gs0 = (warp % WPR) * NS;               // row segment index of this warp's segment 0
+  // SPLIT: fp64 lanes of 4 consecutive k (one segment). Global rows are read
+  // and written with 256-bit accesses (lane offset 4*lane); shared rows keep
+  // a lane's two halves in the row's two halves (lane offset 2*lane, see
+  // sload_split), so every LDS/STS.128 is a conflict-free 512-byte access.
+  constexpr bool SPLIT = sizeof(T) == 8 && K == 4;
+  static_assert(!SPLIT || (NS == 1 && WPR == 1), "split rows: one segment, one warp per row");
+  const int lks = SPLIT ? 2 * lane : lk;  // this lane's offset in a shared row
   const unsigned PLN = static_cast<unsigned>(a.plane);
 
   // Rows of this warp: region row r = wrow + rr. Element offsets within a
@@ -354,6 +426,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     gjm[rr] = static_cast<unsigned>((j == 0 ? m - 1 : j - 1) * L + lk);
     gjp[rr] = static_cast<unsigned>((j == m - 1 ? 0 : j + 1) * L + lk);
   }
+  auto SLD = [](const T* p) {
+    if constexpr (SPLIT) return sload_split<T, K, L>(p);
+    else return sload<T, K>(p);
+  };
+  auto SST = [](T* p, const V& v) {
+    if constexpr (SPLIT) sstore_split<T, K, L>(p, v);
+    else vstore(p, v);
+  };
   auto slot3 = [](int p) { return C::NX1 == 4 ? ((p + 8) & 3) : (p + 6) % 3; };  // p >= -3
   // element offset of plane p of the padded slab
   auto pl = [&](int p) -> unsigned {
@@ -457,6 +537,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   constexpr bool TMS = TMM && IMB_TMEM_STAR && MODE != 2;     // psi^n star ring
   constexpr bool TMH = TMM && IMB_TMEM_CACHE;                  // h ring
   constexpr bool TMC = TMH && (!TMWB || MODE == 2);            // v rows ring
+  // TMU (MODE 0/1 with TMWB): the x-face velocity carries (planes t, t+1)
+  // and the x-flux carry live in TMEM too, in the columns a 2-slot star ring
+  // and a 3-slot h ring leave free (star(p) is last read by bounds(p), before
+  // donor(p+2) reuses its slot in the same iteration; h(p) by final(p), before
+  // donor(p+3)). Layout: star [0,32) h [32,56) u [56,72) fx [72,80).
+  constexpr bool TMU = TMWB && MODE != 2 && IMB_TMEM_CARRY;
   __shared__ unsigned s_tmem_base;
   unsigned tm_lane = 0;
   if constexpr (TMM) {
@@ -472,34 +558,68 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     tm_lane = s_tmem_base + (static_cast<unsigned>((warp & 3) * 32) << 16) +
               static_cast<unsigned>(warp >> 2) * (512u / (NW / 4));
   }
-  auto tm_star = [&](int p) { return tm_lane + static_cast<unsigned>((p + 6) % 3) * 16u; };
-  auto tm_h = [&](int p) { return tm_lane + 48u + static_cast<unsigned>((p + 8) & 3) * 8u; };
+  auto tm_star = [&](int p) {
+    return tm_lane + (TMU ? static_cast<unsigned>(p & 1) : static_cast<unsigned>((p + 6) % 3)) * 16u;
+  };
+  auto tm_h = [&](int p) {
+    return TMU ? tm_lane + 32u + static_cast<unsigned>((p + 6) % 3) * 8u
+               : tm_lane + 48u + static_cast<unsigned>((p + 8) & 3) * 8u;
+  };
+  auto tm_u = [&](int p) { return tm_lane + 56u + static_cast<unsigned>(p & 1) * 8u; };
+  auto tm_fx = [&]() { return tm_lane + 72u; };
   auto tm_v = [&](int p) { return tm_lane + (MODE == 2 ? 0u : 80u) + static_cast<unsigned>((p + 6) % 3) * 16u; };
   auto tm_b = [&](int p) { return tm_lane + 80u + static_cast<unsigned>(p & 1) * 16u; };
   auto tm_w = [&](int p) { return tm_lane + 112u + static_cast<unsigned>(p & 1) * 8u; };
-  // load a V from 4 TMEM columns (after tmem_wait_ld)
-  auto vfrom = [](const unsigned* w) {
-    V r;
-    double d[2];
-    unpack2(w, d);
-    r.e[0] = d[0];
-    r.e[1] = d[1];
-    return r;
+  // A V is CW = 2K TMEM columns; every ring slot holds NC*K = 4 doubles of
+  // a row (8 columns) or two such rows / a max-min pair (16 columns).
+  constexpr int CW = 2 * K;
+  static_assert(!TMM || NC * K == 4, "TMEM rings hold 4 doubles per row and lane");
+  auto vfrom = [](const unsigned* w) { return unpackv<T, K>(w); };
+  auto tst = [&](unsigned addr, const V& x) {  // one V -> CW columns
+    unsigned w[CW];
+    packv(x, w);
+    tmem_st<CW>(addr, w);
   };
-  // TMWB: z-velocities of plane p, segment c, and their k+1 neighbours. The
-  // two segments of a row are one TMEM load; lane 31's neighbour is lane 0's
-  // first cell of the next segment (of segment 0 after the last: periodic),
-  // which lane 0 offers in place of its own to the single shuffle.
+  auto tst2 = [&](unsigned addr, const V& x, const V& y) {  // two Vs -> 2 CW columns
+    unsigned w[2 * CW];
+    packv(x, w);
+    packv(y, w + CW);
+    tmem_st<2 * CW>(addr, w);
+  };
+  auto tld = [&](unsigned addr) {
+    unsigned w[CW];
+    tmem_ld<CW>(addr, w);
+    tmem_wait_ld(w);
+    return vfrom(w);
+  };
+  auto tld2 = [&](unsigned addr, V& x, V& y) {
+    unsigned w[2 * CW];
+    tmem_ld<2 * CW>(addr, w);
+    tmem_wait_ld(w);
+    x = vfrom(w);
+    y = vfrom(w + CW);
+  };
+  // TMWB: z-velocities of plane p, segment c, and their k+1 neighbours. With
+  // two segments of a row (K = 2) the row is one TMEM load; lane 31's
+  // neighbour is lane 0's first cell of the next segment (of segment 0 after
+  // the last: periodic), which lane 0 offers in place of its own to the single
+  // shuffle. With one segment (K = 4) the shuffle closes the periodic row.
   auto tm_wk = [&](int p, int c, V& wc, V& wcp) {
-    static_assert(!TMWB || (NC == 2 && K == 2), "TMWB is written for 2 segments of 2 doubles");
-    unsigned t8[8];
-    tmem_ld8(tm_w(p), t8);
-    tmem_wait_ld(t8);
-    const V s0 = vfrom(t8), s1 = vfrom(t8 + 4);
-    wc = c == 0 ? s0 : s1;
-    const T offer = lane == 0 ? (c == 0 ? s1.e[0] : s0.e[0]) : wc.e[0];
-    wcp.e[0] = wc.e[1];
-    wcp.e[1] = __shfl_sync(kFull, offer, (lane + 1) & 31);
+    if constexpr (NC == 1) {
+      wc = tld(tm_w(p));
+#pragma unroll
+      for (int e = 0; e + 1 < K; ++e) wcp.e[e] = wc.e[e + 1];
+      wcp.e[K - 1] = __shfl_sync(kFull, wc.e[0], (lane + 1) & 31);
+    } else {
+      static_assert(!TMWB || NC == 1 || (NC == 2 && K == 2), "TMWB: 1 segment, or 2 of 2 doubles");
+      V s0, s1;
+      tld2(tm_w(p), s0, s1);
+      wc = c == 0 ? s0 : s1;
+      const T offer = lane == 0 ? (c == 0 ? s1.e[0] : s0.e[0]) : wc.e[0];
+#pragma unroll
+      for (int e = 0; e + 1 < K; ++e) wcp.e[e] = wc.e[e + 1];
+      wcp.e[K - 1] = __shfl_sync(kFull, offer, (lane + 1) & 31);
+    }
   };
 
   // psi^n star extrema (STARC): of plane t+1 (nmx), t+2 (nmx_mid, EARLY) and
@@ -515,24 +635,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       for (int c = 0; c < NC; ++c) {
         const int rr = c / NS, so = sgo(c);
         const unsigned ij = px + gj[rr];
-        vstore(dst + (wrow + rr) * L + lk + so, vload<T, K>(a.x + ij + so));
+        SST(dst + (wrow + rr) * L + lks + so, vload<T, K>(a.x + ij + so));
         if constexpr (STARC) {
           nmx_new[c] = vload<T, K>(a.mxo + ij + so);
           nmn_new[c] = vload<T, K>(a.mno + ij + so);
         }
-        if constexpr (TMH) {  // the h and v rings, as the donor of MODE 0/1 fills them
-          unsigned w4[4];
-          const V hc = vload<T, K>(a.h + ij + so);
-          pack2(reinterpret_cast<const double(&)[2]>(hc.e), w4);
-          tmem_st4(tm_h(p) + 4u * static_cast<unsigned>(c), w4);
-        }
-        if constexpr (TMC) {
-          unsigned w8[8];
-          const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
-          pack2(reinterpret_cast<const double(&)[2]>(vc.e), w8);
-          pack2(reinterpret_cast<const double(&)[2]>(vp.e), w8 + 4);
-          tmem_st8(tm_v(p) + 8u * static_cast<unsigned>(c), w8);
-        }
+        if constexpr (TMH)  // the h and v rings, as the donor of MODE 0/1 fills them
+          tst(tm_h(p) + CW * static_cast<unsigned>(c), vload<T, K>(a.h + ij + so));
+        if constexpr (TMC)
+          tst2(tm_v(p) + 2 * CW * static_cast<unsigned>(c), vload<T, K>(a.v + ij + so),
+               vload<T, K>(a.v + (px + gjp[rr]) + so));
       }
       if constexpr (TMH) tmem_wait_st();
       return;
@@ -576,17 +688,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       }
       const V uc = vload<T, K>(a.u + ij + so), up = vload<T, K>(a.u + (ij + PLN) + so);
       const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
-      if constexpr (TMH) {  // segment c: h -> [4c, 4c+4) of its slot
-        unsigned w4[4];
-        pack2(reinterpret_cast<const double(&)[2]>(hc.e), w4);
-        tmem_st4(tm_h(p) + 4u * static_cast<unsigned>(c), w4);
-      }
-      if constexpr (TMC) {  // v rows j, j+1 -> [8c, 8c+8)
-        unsigned w8[8];
-        pack2(reinterpret_cast<const double(&)[2]>(vc.e), w8);
-        pack2(reinterpret_cast<const double(&)[2]>(vp.e), w8 + 4);
-        tmem_st8(tm_v(p) + 8u * static_cast<unsigned>(c), w8);
-      }
+      if constexpr (TMH) tst(tm_h(p) + CW * static_cast<unsigned>(c), hc);  // h -> [CW c, CW c + CW)
+      if constexpr (TMC) tst2(tm_v(p) + 2 * CW * static_cast<unsigned>(c), vc, vp);  // v rows j, j+1
       const T* W = a.w + ij + so;
       const V wc = vload<T, K>(W);
       const V wp = KPG(c, wc, W);
@@ -609,18 +712,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
                                  tmin(tmin(yp.e[e], zm.e[e]), zp.e[e]));
         }
       }
-      vstore(dst + r * L + lk + so, res);
-      if constexpr (TMS) {  // segment c -> columns [8c, 8c+8): max (K doubles), then min
-        unsigned tv[8];
-#pragma unroll
-        for (int e = 0; e < K; ++e) {
-          tv[2 * e] = static_cast<unsigned>(__double2loint(nmx_new[c].e[e]));
-          tv[2 * e + 1] = static_cast<unsigned>(__double2hiint(nmx_new[c].e[e]));
-          tv[4 + 2 * e] = static_cast<unsigned>(__double2loint(nmn_new[c].e[e]));
-          tv[4 + 2 * e + 1] = static_cast<unsigned>(__double2hiint(nmn_new[c].e[e]));
-        }
-        tmem_st8(tm_star(p) + 8u * static_cast<unsigned>(c), tv);
-      }
+      SST(dst + r * L + lks + so, res);
+      if constexpr (TMS)  // segment c -> columns [2CW c, 2CW c + 2CW): max, then min
+        tst2(tm_star(p) + 2 * CW * static_cast<unsigned>(c), nmx_new[c], nmn_new[c]);
     }
     if constexpr (TMS) tmem_wait_st();
   };
@@ -639,18 +733,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (r < 1) continue;  // warp-uniform
       const bool row_u = r < RR - 1;  // x/z faces (y faces: every r >= 1)
       const unsigned i1 = p1 + gj[rr], i2 = p2 + gj[rr];
-      const int so = r * L + lk + sg;  // smem offset of this vector
-      const V x1 = sload<T, K>(s1 + so);
+      const int so = r * L + lks + sg;  // smem offset of this vector
+      const V x1 = SLD(s1 + so);
       const V a1 = vabs(x1);
-      const V a1m = vabs(sload<T, K>(s1 + so - L));
+      const V a1m = vabs(SLD(s1 + so - L));
       const T* U2 = a.u + i2 + sg;
       const V u2c = vload<T, K>(U2);
       // v rows j, j+1 and h row j of planes pb, pb+1 (TMEM ring or L2)
       V h1c, h2, v1, v2, v1p, v2p;
+      const unsigned cw = CW * static_cast<unsigned>(c);
       if constexpr (TMH && !TMC) {
-        unsigned ha[4], hb[4];
-        tmem_ld4(tm_h(pb) + 4u * static_cast<unsigned>(c), ha);
-        tmem_ld4(tm_h(pb + 1) + 4u * static_cast<unsigned>(c), hb);
+        unsigned ha[CW], hb[CW];
+        tmem_ld<CW>(tm_h(pb) + cw, ha);
+        tmem_ld<CW>(tm_h(pb + 1) + cw, hb);
         v1 = vload<T, K>(a.v + i1 + sg);
         v2 = vload<T, K>(a.v + i2 + sg);
         v1p = vload<T, K>(a.v + (p1 + gjp[rr]) + sg);
@@ -660,19 +755,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         h1c = vfrom(ha);
         h2 = vfrom(hb);
       } else if constexpr (TMC) {
-        unsigned wa[8], wb[8], ha[4], hb[4];
-        tmem_ld8(tm_v(pb) + 8u * static_cast<unsigned>(c), wa);
-        tmem_ld8(tm_v(pb + 1) + 8u * static_cast<unsigned>(c), wb);
-        tmem_ld4(tm_h(pb) + 4u * static_cast<unsigned>(c), ha);
-        tmem_ld4(tm_h(pb + 1) + 4u * static_cast<unsigned>(c), hb);
+        unsigned wa[2 * CW], wb[2 * CW], ha[CW], hb[CW];
+        tmem_ld<2 * CW>(tm_v(pb) + 2 * cw, wa);
+        tmem_ld<2 * CW>(tm_v(pb + 1) + 2 * cw, wb);
+        tmem_ld<CW>(tm_h(pb) + cw, ha);
+        tmem_ld<CW>(tm_h(pb + 1) + cw, hb);
         tmem_wait_ld(wa);
         tmem_wait_ld(wb);  // (already complete: these only order the register uses)
         tmem_wait_ld(ha);
         tmem_wait_ld(hb);
         v1 = vfrom(wa);
-        v1p = vfrom(wa + 4);
+        v1p = vfrom(wa + CW);
         v2 = vfrom(wb);
-        v2p = vfrom(wb + 4);
+        v2p = vfrom(wb + CW);
         h1c = vfrom(ha);
         h2 = vfrom(hb);
       } else {
@@ -685,14 +780,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       }
       const V a1km = vabs(KMS(c, x1, s1 + so));
       if (row_u) {  // x-face between planes pb and pb+1 of this column
-        const V x2 = sload<T, K>(s2 + so);
+        const V x2 = SLD(s2 + so);
         const V a2 = vabs(x2);
         const V a1kp = vabs(KPS(c, x1, s1 + so));
         const V a2kp = vabs(KPS(c, x2, s2 + so)), a2km = vabs(KMS(c, x2, s2 + so));
         V bp, bm, cp, cm, Vs, Ws;
         {
-          const V a1p = vabs(sload<T, K>(s1 + so + L)), a2p = vabs(sload<T, K>(s2 + so + L));
-          const V a2m = vabs(sload<T, K>(s2 + so - L));
+          const V a1p = vabs(SLD(s1 + so + L)), a2p = vabs(SLD(s2 + so + L));
+          const V a2m = vabs(SLD(s2 + so - L));
 #pragma unroll
           for (int e = 0; e < K; ++e) {
             bp.e[e] = a1p.e[e] + a2p.e[e];
@@ -713,23 +808,26 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #pragma unroll
           for (int e = 0; e < K; ++e) Ws.e[e] = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
         }
+        V ures;
 #pragma unroll
         for (int e = 0; e < K; ++e)
-          ut[c].e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e], bp.e[e],
-                                      bm.e[e], Vs.e[e], cp.e[e], cm.e[e], Ws.e[e]);
+          ures.e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e], bp.e[e],
+                                     bm.e[e], Vs.e[e], cp.e[e], cm.e[e], Ws.e[e]);
+        if constexpr (TMU) tst(tm_u(pb) + CW * static_cast<unsigned>(c), ures);
+        else ut[c] = ures;
       }
       if (only_u) continue;
-      const V x0 = sload<T, K>(s0 + so);
-      const V x2 = sload<T, K>(s2 + so);
+      const V x0 = SLD(s0 + so);
+      const V x2 = SLD(s2 + so);
       const T* U1 = a.u + i1 + sg;
       const V u1c = vload<T, K>(U1);
       const T* W1 = a.w + i1 + sg;
       const V w1 = vload<T, K>(W1);
       {  // y-face between rows r-1 and r of plane pb
-        const V x1m = sload<T, K>(s1 + so - L);
+        const V x1m = SLD(s1 + so - L);
         V bp, bm, cp, cm, Us, Ws;
         {
-          const V a0m = vabs(sload<T, K>(s0 + so - L)), a2m = vabs(sload<T, K>(s2 + so - L));
+          const V a0m = vabs(SLD(s0 + so - L)), a2m = vabs(SLD(s2 + so - L));
           const V a1mkp = vabs(KPS(c, x1m, s1 + so - L));
           const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
           const V a1kp = vabs(KPS(c, x1, s1 + so));
@@ -759,13 +857,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         for (int e = 0; e < K; ++e)
           res.e[e] = pseudo_face<T>(v1.e[e], h1m.e[e], h1c.e[e], a1.e[e], a1m.e[e], bp.e[e],
                                     bm.e[e], Us.e[e], cp.e[e], cm.e[e], Ws.e[e]);
-        vstore(vdst + so, res);
+        SST(vdst + so, res);
       }
       if (row_u) {  // z-face between k-1 and k
         V bp, bm, cp, cm, Us, Vs;
         {
-          const V x1p = sload<T, K>(s1 + so + L);
-          const V x1m = sload<T, K>(s1 + so - L);
+          const V x1p = SLD(s1 + so + L);
+          const V x1m = SLD(s1 + so - L);
           const V a1pkm = vabs(KMS(c, x1p, s1 + so + L));
           const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
           const V a2km = vabs(KMS(c, x2, s2 + so)), a0km = vabs(KMS(c, x0, s0 + so));
@@ -797,16 +895,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           res.e[e] = pseudo_face<T>(w1.e[e], h1km.e[e], h1c.e[e], a1.e[e], a1km.e[e], bp.e[e],
                                     bm.e[e], Us.e[e], cp.e[e], cm.e[e], Vs.e[e]);
         if constexpr (TMWB) {
-          unsigned w4[4];
-          pack2(reinterpret_cast<const double(&)[2]>(res.e), w4);
-          tmem_st4(tm_w(pb) + 4u * static_cast<unsigned>(c), w4);
+          tst(tm_w(pb) + CW * static_cast<unsigned>(c), res);
         } else {
-          vstore(wdst + so, res);
+          SST(wdst + so, res);
         }
       }
     }
     if constexpr (TMWB) {
-      if (!only_u) tmem_wait_st();
+      if (!only_u || TMU) tmem_wait_st();
     }
   };
 
@@ -927,25 +1023,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const int rr = c / NS, sg = sgo(c);
           const int r = wrow + rr;
           if (r < 1 || r >= RR - 1) continue;
-          const int so = r * L + lk + sg;
+          const int so = r * L + lks + sg;
           const unsigned i1 = q1 + gj[rr];
-          const V xc = sload<T, K>(s1 + so);
-          const V xm = sload<T, K>(s0 + so), xp = sload<T, K>(s2 + so);
-          const V ym = sload<T, K>(s1 + so - L), yp = sload<T, K>(s1 + so + L);
+          const V xc = SLD(s1 + so);
+          const V xm = SLD(s0 + so), xp = SLD(s2 + so);
+          const V ym = SLD(s1 + so - L), yp = SLD(s1 + so + L);
           const V zm = KMS(c, xc, s1 + so), zp = KPS(c, xc, s1 + so);
           V mx, mn;
           if constexpr (STARC) {
             mx = nmx[c];
             mn = nmn[c];
           } else if constexpr (TMS) {  // (warp-uniform here: the whole warp owns row r)
-            unsigned tv[8];
-            tmem_ld8(tm_star(p1) + 8u * static_cast<unsigned>(c), tv);
-            tmem_wait_ld(tv);
-#pragma unroll
-            for (int e = 0; e < K; ++e) {
-              mx.e[e] = __hiloint2double(static_cast<int>(tv[2 * e + 1]), static_cast<int>(tv[2 * e]));
-              mn.e[e] = __hiloint2double(static_cast<int>(tv[2 * e + 5]), static_cast<int>(tv[2 * e + 4]));
-            }
+            tld2(tm_star(p1) + 2 * CW * static_cast<unsigned>(c), mx, mn);
           } else if constexpr (MODE == 2) {  // bounds of the previous pass
             mx = vload<T, K>(a.mxo + i1 + sg);
             mn = vload<T, K>(a.mno + i1 + sg);
@@ -963,22 +1052,29 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
                              tmin(tmin(nyp.e[e], nzm.e[e]), nzp.e[e]));
             }
           }
-          const V va = sload<T, K>(vA + so), vap = sload<T, K>(vA + so + L);
+          const V va = SLD(vA + so), vap = SLD(vA + so + L);
           V wa, wap;
           if constexpr (TMWB) {
             tm_wk(p1, c, wa, wap);
           } else {
-            wa = sload<T, K>(wA + so);
+            wa = SLD(wA + so);
             wap = KPS(c, wa, wA + so);
           }
           V hc;
           if constexpr (TMH) {
-            unsigned w4[4];
-            tmem_ld4(tm_h(p1) + 4u * static_cast<unsigned>(c), w4);
-            tmem_wait_ld(w4);
-            hc = vfrom(w4);
+            hc = tld(tm_h(p1) + CW * static_cast<unsigned>(c));
           } else {
             hc = STG ? sload<T, K>(hrow(p1, r) + sg) : vload<T, K>(a.h + i1 + sg);
+          }
+          V uL = ucar[c], uR = ufresh[c];  // x-face velocities (t|t+1), (t+1|t+2)
+          if constexpr (TMU) {
+            unsigned wl[CW], wr[CW];
+            tmem_ld<CW>(tm_u(t) + CW * static_cast<unsigned>(c), wl);
+            tmem_ld<CW>(tm_u(p1) + CW * static_cast<unsigned>(c), wr);
+            tmem_wait_ld(wl);
+            tmem_wait_ld(wr);
+            uL = vfrom(wl);
+            uR = vfrom(wr);
           }
           V bu, bd, his, los;
 #pragma unroll
@@ -990,8 +1086,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
                               tmin(tmin(ym.e[e], yp.e[e]), tmin(zm.e[e], zp.e[e])));
             his.e[e] = hi;
             los.e[e] = lo;
-            const T axl = upflux(xm.e[e], x0, ucar[c].e[e]);
-            const T axr = upflux(x0, xp.e[e], ufresh[c].e[e]);
+            const T axl = upflux(xm.e[e], x0, uL.e[e]);
+            const T axr = upflux(x0, xp.e[e], uR.e[e]);
             const T ayl = upflux(ym.e[e], x0, va.e[e]);
             const T ayr = upflux(x0, yp.e[e], vap.e[e]);
             const T azl = upflux(zm.e[e], x0, wa.e[e]);
@@ -1014,13 +1110,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               bd.e[e] = qdiv((x0 - lo) * hc.e[e], dou);
             }
           }
-          vstore(buA + so, bu);
-          vstore(bdA + so, bd);
+          SST(buA + so, bu);
+          SST(bdA + so, bd);
           if constexpr (TMWB) {  // this thread's betas of plane t+1, for its own x-face limit next iteration
-            unsigned t8[8];
-            pack2(reinterpret_cast<const double(&)[2]>(bu.e), t8);
-            pack2(reinterpret_cast<const double(&)[2]>(bd.e), t8 + 4);
-            tmem_st8(tm_b(p1) + 8u * static_cast<unsigned>(c), t8);
+            tst2(tm_b(p1) + 2 * CW * static_cast<unsigned>(c), bu, bd);
           }
           if constexpr (MODE == 1) {  // bounds for the next pass
             if (keep(t, r)) {
@@ -1049,16 +1142,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const int rr = c / NS, sg = sgo(c);
           const int r = wrow + rr;
           if (r < 2 || r >= RR - 1) continue;
-          const int so = r * L + lk + sg;
-          const V bu = sload<T, K>(buA + so), bd = sload<T, K>(bdA + so);
+          const int so = r * L + lks + sg;
+          const V bu = SLD(buA + so), bd = SLD(bdA + so);
           {
-            const V va = sload<T, K>(vA + so);
-            const V bum = sload<T, K>(buA + so - L), bdm = sload<T, K>(bdA + so - L);
+            const V va = SLD(vA + so);
+            const V bum = SLD(buA + so - L), bdm = SLD(bdA + so - L);
             V res;
 #pragma unroll
             for (int e = 0; e < K; ++e)
               res.e[e] = limit_sel(va.e[e], bdm.e[e], bu.e[e], bum.e[e], bd.e[e]);
-            vstore(vA + so, res);
+            SST(vA + so, res);
             if constexpr (MODE == 1) {
               if (keep(t, r)) vstore(a.vo + (q1 + gj[rr]) + sg, res);
             }
@@ -1068,36 +1161,35 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           {
             V wa, buo, bdo;
             if constexpr (TMWB) {
-              unsigned t8[8], w4[4];
-              tmem_ld8(tm_b(t) + 8u * static_cast<unsigned>(c), t8);
-              tmem_ld4(tm_w(p1) + 4u * static_cast<unsigned>(c), w4);
+              unsigned t8[2 * CW], w4[CW];
+              tmem_ld<2 * CW>(tm_b(t) + 2 * CW * static_cast<unsigned>(c), t8);
+              tmem_ld<CW>(tm_w(p1) + CW * static_cast<unsigned>(c), w4);
               tmem_wait_ld(t8);
               tmem_wait_ld(w4);
               buo = vfrom(t8);
-              bdo = vfrom(t8 + 4);
+              bdo = vfrom(t8 + CW);
               wa = vfrom(w4);
             } else {
-              wa = sload<T, K>(wA + so);
-              buo = sload<T, K>(buB + so);
-              bdo = sload<T, K>(bdB + so);
+              wa = SLD(wA + so);
+              buo = SLD(buB + so);
+              bdo = SLD(bdB + so);
             }
             const V bukm = KMS(c, bu, buA + so), bdkm = KMS(c, bd, bdA + so);
-            const V xc = sload<T, K>(s0 + so);
-            const V x1 = sload<T, K>(s1 + so);
+            const V xc = SLD(s0 + so);
+            const V x1 = SLD(s1 + so);
+            const V uc = TMU ? tld(tm_u(t) + CW * static_cast<unsigned>(c)) : ucar[c];
             V wres, uls;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
               wres.e[e] = limit_sel(wa.e[e], bdkm.e[e], bu.e[e], bukm.e[e], bd.e[e]);
-              const T ul = limit_sel(ucar[c].e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
+              const T ul = limit_sel(uc.e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
               uls.e[e] = ul;
               fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
             }
             if constexpr (TMWB) {
-              unsigned w4[4];
-              pack2(reinterpret_cast<const double(&)[2]>(wres.e), w4);
-              tmem_st4(tm_w(p1) + 4u * static_cast<unsigned>(c), w4);
+              tst(tm_w(p1) + CW * static_cast<unsigned>(c), wres);
             } else {
-              vstore(wA + so, wres);
+              SST(wA + so, wres);
             }
             if constexpr (MODE == 1) {
               if (keep(t, r)) {
@@ -1107,26 +1199,24 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             }
           }
           if (emit) {
-            const V xc = sload<T, K>(s0 + so);
-            const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
+            const V xc = SLD(s0 + so);
+            const V ym = SLD(s0 + so - L), yp = SLD(s0 + so + L);
             const V zm = KMS(c, xc, s0 + so), zp = KPS(c, xc, s0 + so);
-            const V vb = sload<T, K>(vB + so), vbp = sload<T, K>(vB + so + L);
+            const V vb = SLD(vB + so), vbp = SLD(vB + so + L);
             V wb, wbp;
             if constexpr (TMWB) {
               tm_wk(t, c, wb, wbp);
             } else {
-              wb = sload<T, K>(wB + so);
+              wb = SLD(wB + so);
               wbp = KPS(c, wb, wB + so);
             }
             V hc;
             if constexpr (TMH) {
-              unsigned w4[4];
-              tmem_ld4(tm_h(t) + 4u * static_cast<unsigned>(c), w4);
-              tmem_wait_ld(w4);
-              hc = vfrom(w4);
+              hc = tld(tm_h(t) + CW * static_cast<unsigned>(c));
             } else {
               hc = STG ? sload<T, K>(hrow(t, r) + sg) : vload<T, K>(a.h + (q0 + gj[rr]) + sg);
             }
+            const V fxl = TMU ? tld(tm_fx() + CW * static_cast<unsigned>(c)) : fxc[c];
             V res;
 #pragma unroll
             for (int e = 0; e < K; ++e) {
@@ -1135,13 +1225,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               const T fyr = upflux(x0, yp.e[e], vbp.e[e]);
               const T fzl = upflux(zm.e[e], x0, wb.e[e]);
               const T fzr = upflux(x0, zp.e[e], wbp.e[e]);
-              const T div = ((fxr.e[e] - fxc[c].e[e]) + (fyr - fyl)) + (fzr - fzl);
+              const T div = ((fxr.e[e] - fxl.e[e]) + (fyr - fyl)) + (fzr - fzl);
               res.e[e] = x0 - qdiv(div, hc.e[e]);
             }
             const int j = j0 + r - 2;
             if (j < m) vstore(a.out + (q0 + gj[rr]) + sg, res);
           }
-          fxc[c] = fxr;
+          if constexpr (TMU) tst(tm_fx() + CW * static_cast<unsigned>(c), fxr);
+          else fxc[c] = fxr;
         }
       }
       if constexpr (TMWB) tmem_wait_st();
@@ -1181,13 +1272,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const int rr = c / NS, sg = sgo(c);
         const int r = wrow + rr;
         if (r < 1 || r >= RR - 1) continue;
-        const int so = r * L + lk + sg;
-        const V xc = sload<T, K>(s0 + so);
-        const V xm = sload<T, K>(sm1 + so), xp = sload<T, K>(s1 + so);
-        const V ym = sload<T, K>(s0 + so - L), yp = sload<T, K>(s0 + so + L);
+        const int so = r * L + lks + sg;
+        const V xc = SLD(s0 + so);
+        const V xm = SLD(sm1 + so), xp = SLD(s1 + so);
+        const V ym = SLD(s0 + so - L), yp = SLD(s0 + so + L);
         const V zm = KMS(c, xc, s0 + so), zp = KPS(c, xc, s0 + so);
-        const V vv = sload<T, K>(s_v + so), vvp = sload<T, K>(s_v + so + L);
-        const V ww = sload<T, K>(s_w + so);
+        const V vv = SLD(s_v + so), vvp = SLD(s_v + so + L);
+        const V ww = SLD(s_w + so);
         const V wwp = KPS(c, ww, s_w + so);
         const V hc = vload<T, K>(a.h + (q0 + gj[rr]) + sg);
         V res;
@@ -1379,7 +1470,7 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
       if constexpr (D)
         return launch_cfg<T, 128, 1, IMB_F64_WPR2_NW, 1, NONOS, false, MODE, false, 2>(fs, a, num_sms, st);
 #endif
-      return launch_cfg<T, 128, 1, 16, D ? 2 : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
+      return launch_cfg<T, 128, 1, 16, D ? IMB_F64_NS : 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 64: return launch_cfg<T, 64, 2, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     case 32: return launch_cfg<T, 32, 4, 16, 1, NONOS, !D, MODE>(fs, a, num_sms, st);
     default: return 0;

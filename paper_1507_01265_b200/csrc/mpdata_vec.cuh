@@ -89,10 +89,9 @@ struct Vec {
 template <class T, int K>
 __device__ __forceinline__ Vec<T, K> vload(const T* p) {  // global, read-only path
   Vec<T, K> r;
-  if constexpr (sizeof(T) == 8 && K == 4) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
+  if constexpr (sizeof(T) == 8 && K == 4) {  // one 256-bit load (sm_100: global only)
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(r.e[0]), "=d"(r.e[1]), "=d"(r.e[2]), "=d"(r.e[3]) : "l"(p));
   } else if constexpr (sizeof(T) == 8 && K == 2) {
     const double2 a = __ldg(reinterpret_cast<const double2*>(p));
     r.e[0] = a.x; r.e[1] = a.y;
@@ -113,9 +112,8 @@ template <class T, int K>
 __device__ __forceinline__ Vec<T, K> vload_cg(const T* p) {
   Vec<T, K> r;
   if constexpr (sizeof(T) == 8 && K == 4) {
-    const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
-    r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(r.e[0]), "=d"(r.e[1]), "=d"(r.e[2]), "=d"(r.e[3]) : "l"(p) : "memory");
   } else if constexpr (sizeof(T) == 8 && K == 2) {
     const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
     r.e[0] = a.x; r.e[1] = a.y;
@@ -159,9 +157,10 @@ __device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or
 #ifdef IMB_CHECKED
   if (__isShared(p)) check_shared(p, sizeof(T) * K);
 #endif
-  if constexpr (sizeof(T) == 8 && K == 4) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v.e[2], v.e[3]);
+  if constexpr (sizeof(T) == 8 && K == 4) {  // global only: one 256-bit store (shared: sstore)
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.e[0]), "d"(v.e[1]),
+                 "d"(v.e[2]), "d"(v.e[3])
+                 : "memory");
   } else if constexpr (sizeof(T) == 8 && K == 2) {
     reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
   } else if constexpr (sizeof(T) == 4 && K == 4) {
@@ -171,6 +170,30 @@ __device__ __forceinline__ void vstore(T* p, const Vec<T, K>& v) {  // shared or
   } else {
     p[0] = v.e[0];
   }
+}
+
+// Shared-memory rows of fp64 lanes holding 4 consecutive k (SPLIT layout):
+// a lane's first two doubles sit in the row's first half at 16 B * lane, its
+// last two in the second half (L/2 doubles on), so each half is one
+// conflict-free 512-byte LDS.128/STS.128 wavefront set. p = the row + 2 * lane.
+template <class T, int K, int L>
+__device__ __forceinline__ Vec<T, K> sload_split(const T* p) {
+  static_assert(sizeof(T) == 8 && K == 4, "split rows hold 4 doubles per lane");
+  check_shared(p, 16);
+  check_shared(p + L / 2, 16);
+  Vec<T, K> r;
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p + L / 2)[0];
+  r.e[0] = a.x; r.e[1] = a.y; r.e[2] = b.x; r.e[3] = b.y;
+  return r;
+}
+template <class T, int K, int L>
+__device__ __forceinline__ void sstore_split(T* p, const Vec<T, K>& v) {
+  static_assert(sizeof(T) == 8 && K == 4, "split rows hold 4 doubles per lane");
+  check_shared(p, 16);
+  check_shared(p + L / 2, 16);
+  reinterpret_cast<double2*>(p)[0] = make_double2(v.e[0], v.e[1]);
+  reinterpret_cast<double2*>(p + L / 2)[0] = make_double2(v.e[2], v.e[3]);
 }
 
 template <class T, int K>
