@@ -235,6 +235,9 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_TMEM_CARRY  // x-face velocity and x-flux carries in tensor memory (fp64)
 #define IMB_TMEM_CARRY 1
 #endif
+#ifndef IMB_M2_TMU  // IORD=3 pass 3 (MODE 2): the carries in TMEM instead of the v ring
+#define IMB_M2_TMU 1
+#endif
 
 // Instantiations that use tensor memory as per-thread storage: the fp64
 // limiter shapes with one 4-double lane vector per row (see k_fused: the
@@ -536,13 +539,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   constexpr bool TMM = use_tmem<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
   constexpr bool TMS = TMM && IMB_TMEM_STAR && MODE != 2;     // psi^n star ring
   constexpr bool TMH = TMM && IMB_TMEM_CACHE;                  // h ring
-  constexpr bool TMC = TMH && (!TMWB || MODE == 2);            // v rows ring
+  constexpr bool TMC = TMH && (!TMWB || (MODE == 2 && !IMB_M2_TMU));  // v rows ring
   // TMU (MODE 0/1 with TMWB): the x-face velocity carries (planes t, t+1)
   // and the x-flux carry live in TMEM too, in the columns a 2-slot star ring
   // and a 3-slot h ring leave free (star(p) is last read by bounds(p), before
   // donor(p+2) reuses its slot in the same iteration; h(p) by final(p), before
   // donor(p+3)). Layout: star [0,32) h [32,56) u [56,72) fx [72,80).
-  constexpr bool TMU = TMWB && MODE != 2 && IMB_TMEM_CARRY;
+  constexpr bool TMU = TMWB && (MODE != 2 || IMB_M2_TMU) && IMB_TMEM_CARRY;
   __shared__ unsigned s_tmem_base;
   unsigned tm_lane = 0;
   if constexpr (TMM) {
