@@ -374,6 +374,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
                 "staged inputs: IORD=2 limiter, one row per warp");
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS, SEG = 32 * K;
   using V = Vec<T, K>;
+  // per-cell arithmetic runs on lane elements: one T, or (fp32) a P2 pair of
+  // adjacent k issued as packed FADD2/FMUL2/FFMA2 (bit-identical rounding)
+  using LN = Lane<T, K>;
+  using S = typename LN::S;
+  constexpr int PK = LN::PK;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   T* s_x1 = sm;                          // psi^(1) slots, by plane
@@ -698,21 +703,22 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       const V wp = KPG(c, wc, W);
       V res;
 #pragma unroll
-      for (int e = 0; e < K; ++e) {
-        const T x0 = xc.e[e];
-        const T fxl = upflux(xm.e[e], x0, uc.e[e]);
-        const T fxr = upflux(x0, xp.e[e], up.e[e]);
-        const T fyl = upflux(ym.e[e], x0, vc.e[e]);
-        const T fyr = upflux(x0, yp.e[e], vp.e[e]);
-        const T fzl = upflux(zm.e[e], x0, wc.e[e]);
-        const T fzr = upflux(x0, zp.e[e], wp.e[e]);
-        const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-        res.e[e] = x0 - qdiv(div, hc.e[e]);
+      for (int e = 0; e < K; e += PK) {
+        auto g = [e](const V& v) { return LN::get(v, e); };
+        const S x0 = g(xc);
+        const S fxl = upflux(g(xm), x0, g(uc));
+        const S fxr = upflux(x0, g(xp), g(up));
+        const S fyl = upflux(g(ym), x0, g(vc));
+        const S fyr = upflux(x0, g(yp), g(vp));
+        const S fzl = upflux(g(zm), x0, g(wc));
+        const S fzr = upflux(x0, g(zp), g(wp));
+        const S div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
+        LN::put(res, e, x0 - qdiv(div, g(hc)));
         if constexpr (NONOS && (STARC || TMS)) {
-          nmx_new[c].e[e] = tmax(tmax(tmax(x0, xm.e[e]), tmax(xp.e[e], ym.e[e])),
-                                 tmax(tmax(yp.e[e], zm.e[e]), zp.e[e]));
-          nmn_new[c].e[e] = tmin(tmin(tmin(x0, xm.e[e]), tmin(xp.e[e], ym.e[e])),
-                                 tmin(tmin(yp.e[e], zm.e[e]), zp.e[e]));
+          LN::put(nmx_new[c], e, tmax(tmax(tmax(x0, g(xm)), tmax(g(xp), g(ym))),
+                                      tmax(tmax(g(yp), g(zm)), g(zp))));
+          LN::put(nmn_new[c], e, tmin(tmin(tmin(x0, g(xm)), tmin(g(xp), g(ym))),
+                                      tmin(tmin(g(yp), g(zm)), g(zp))));
         }
       }
       SST(dst + r * L + lks + so, res);
@@ -792,16 +798,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const V a1p = vabs(SLD(s1 + so + L)), a2p = vabs(SLD(s2 + so + L));
           const V a2m = vabs(SLD(s2 + so - L));
 #pragma unroll
-          for (int e = 0; e < K; ++e) {
-            bp.e[e] = a1p.e[e] + a2p.e[e];
-            bm.e[e] = a1m.e[e] + a2m.e[e];
-            cp.e[e] = a1kp.e[e] + a2kp.e[e];
-            cm.e[e] = a1km.e[e] + a2km.e[e];
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(bp, e, g(a1p) + g(a2p));
+            LN::put(bm, e, g(a1m) + g(a2m));
+            LN::put(cp, e, g(a1kp) + g(a2kp));
+            LN::put(cm, e, g(a1km) + g(a2km));
           }
         }
         {
 #pragma unroll
-          for (int e = 0; e < K; ++e) Vs.e[e] = (v1.e[e] + v2.e[e]) + (v1p.e[e] + v2p.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(Vs, e, (g(v1) + g(v2)) + (g(v1p) + g(v2p)));
+          }
         }
         {
           const T* W1 = a.w + i1 + sg;
@@ -809,13 +819,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const V w1 = vload<T, K>(W1), w2 = vload<T, K>(W2);
           const V w1p = KPG(c, w1, W1), w2p = KPG(c, w2, W2);
 #pragma unroll
-          for (int e = 0; e < K; ++e) Ws.e[e] = (w1.e[e] + w2.e[e]) + (w1p.e[e] + w2p.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(Ws, e, (g(w1) + g(w2)) + (g(w1p) + g(w2p)));
+          }
         }
         V ures;
 #pragma unroll
-        for (int e = 0; e < K; ++e)
-          ures.e[e] = pseudo_face<T>(u2c.e[e], h1c.e[e], h2.e[e], a2.e[e], a1.e[e], bp.e[e],
-                                     bm.e[e], Vs.e[e], cp.e[e], cm.e[e], Ws.e[e]);
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          LN::put(ures, e, pseudo_face(g(u2c), g(h1c), g(h2), g(a2), g(a1), g(bp), g(bm), g(Vs), g(cp),
+                                       g(cm), g(Ws)));
+        }
         if constexpr (TMU) tst(tm_u(pb) + CW * static_cast<unsigned>(c), ures);
         else ut[c] = ures;
       }
@@ -835,31 +850,40 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
           const V a1kp = vabs(KPS(c, x1, s1 + so));
 #pragma unroll
-          for (int e = 0; e < K; ++e) {
-            bp.e[e] = a2m.e[e] + fabs(x2.e[e]);
-            bm.e[e] = a0m.e[e] + fabs(x0.e[e]);
-            cp.e[e] = a1mkp.e[e] + a1kp.e[e];
-            cm.e[e] = a1mkm.e[e] + a1km.e[e];
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(bp, e, g(a2m) + fabs(g(x2)));
+            LN::put(bm, e, g(a0m) + fabs(g(x0)));
+            LN::put(cp, e, g(a1mkp) + g(a1kp));
+            LN::put(cm, e, g(a1mkm) + g(a1km));
           }
         }
         {
           const V u1m = vload<T, K>(a.u + (p1 + gjm[rr]) + sg), u2m = vload<T, K>(a.u + (p2 + gjm[rr]) + sg);
 #pragma unroll
-          for (int e = 0; e < K; ++e) Us.e[e] = (u1m.e[e] + u1c.e[e]) + (u2m.e[e] + u2c.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(Us, e, (g(u1m) + g(u1c)) + (g(u2m) + g(u2c)));
+          }
         }
         {
           const T* W1m = a.w + (p1 + gjm[rr]) + sg;
           const V w1m = vload<T, K>(W1m);
           const V w1mkp = KPG(c, w1m, W1m), w1kp = KPG(c, w1, W1);
 #pragma unroll
-          for (int e = 0; e < K; ++e) Ws.e[e] = (w1m.e[e] + w1.e[e]) + (w1mkp.e[e] + w1kp.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(Ws, e, (g(w1m) + g(w1)) + (g(w1mkp) + g(w1kp)));
+          }
         }
         const V h1m = STG ? sload<T, K>(hrow(pb, r - 1) + sg) : vload<T, K>(a.h + (p1 + gjm[rr]) + sg);
         V res;
 #pragma unroll
-        for (int e = 0; e < K; ++e)
-          res.e[e] = pseudo_face<T>(v1.e[e], h1m.e[e], h1c.e[e], a1.e[e], a1m.e[e], bp.e[e],
-                                    bm.e[e], Us.e[e], cp.e[e], cm.e[e], Ws.e[e]);
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          LN::put(res, e, pseudo_face(g(v1), g(h1m), g(h1c), g(a1), g(a1m), g(bp), g(bm), g(Us), g(cp),
+                                      g(cm), g(Ws)));
+        }
         SST(vdst + so, res);
       }
       if (row_u) {  // z-face between k-1 and k
@@ -871,17 +895,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
           const V a2km = vabs(KMS(c, x2, s2 + so)), a0km = vabs(KMS(c, x0, s0 + so));
 #pragma unroll
-          for (int e = 0; e < K; ++e) {
-            bp.e[e] = a2km.e[e] + fabs(x2.e[e]);
-            bm.e[e] = a0km.e[e] + fabs(x0.e[e]);
-            cp.e[e] = a1pkm.e[e] + fabs(x1p.e[e]);
-            cm.e[e] = a1mkm.e[e] + a1m.e[e];
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(bp, e, g(a2km) + fabs(g(x2)));
+            LN::put(bm, e, g(a0km) + fabs(g(x0)));
+            LN::put(cp, e, g(a1pkm) + fabs(g(x1p)));
+            LN::put(cm, e, g(a1mkm) + g(a1m));
           }
         }
         {
           const V u2km = KMG(c, u2c, U2), u1km = KMG(c, u1c, U1);
 #pragma unroll
-          for (int e = 0; e < K; ++e) Us.e[e] = (u1km.e[e] + u1c.e[e]) + (u2km.e[e] + u2c.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(Us, e, (g(u1km) + g(u1c)) + (g(u2km) + g(u2c)));
+          }
         }
         {
           const T* V1 = a.v + i1 + sg;
@@ -889,14 +917,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 
           const V v1km = KMG(c, v1, V1), v1pkm = KMG(c, v1p, V1p);
 #pragma unroll
-          for (int e = 0; e < K; ++e) Vs.e[e] = (v1km.e[e] + v1.e[e]) + (v1pkm.e[e] + v1p.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            LN::put(Vs, e, (g(v1km) + g(v1)) + (g(v1pkm) + g(v1p)));
+          }
         }
         const V h1km = STG ? KMS(c, h1c, hrow(pb, r) + sg) : KMG(c, h1c, a.h + i1 + sg);
         V res;
 #pragma unroll
-        for (int e = 0; e < K; ++e)
-          res.e[e] = pseudo_face<T>(w1.e[e], h1km.e[e], h1c.e[e], a1.e[e], a1km.e[e], bp.e[e],
-                                    bm.e[e], Us.e[e], cp.e[e], cm.e[e], Vs.e[e]);
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          LN::put(res, e, pseudo_face(g(w1), g(h1km), g(h1c), g(a1), g(a1km), g(bp), g(bm), g(Us), g(cp),
+                                      g(cm), g(Vs)));
+        }
         if constexpr (TMWB) {
           tst(tm_w(pb) + CW * static_cast<unsigned>(c), res);
         } else {
@@ -1081,36 +1114,38 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
           V bu, bd, his, los;
 #pragma unroll
-          for (int e = 0; e < K; ++e) {
-            const T x0 = xc.e[e];
-            const T hi = tmax(tmax(tmax(mx.e[e], x0), tmax(xm.e[e], xp.e[e])),
-                              tmax(tmax(ym.e[e], yp.e[e]), tmax(zm.e[e], zp.e[e])));
-            const T lo = tmin(tmin(tmin(mn.e[e], x0), tmin(xm.e[e], xp.e[e])),
-                              tmin(tmin(ym.e[e], yp.e[e]), tmin(zm.e[e], zp.e[e])));
-            his.e[e] = hi;
-            los.e[e] = lo;
-            const T axl = upflux(xm.e[e], x0, uL.e[e]);
-            const T axr = upflux(x0, xp.e[e], uR.e[e]);
-            const T ayl = upflux(ym.e[e], x0, va.e[e]);
-            const T ayr = upflux(x0, yp.e[e], vap.e[e]);
-            const T azl = upflux(zm.e[e], x0, wa.e[e]);
-            const T azr = upflux(x0, zp.e[e], wap.e[e]);
+          for (int e = 0; e < K; e += PK) {
+            auto g = [e](const V& v) { return LN::get(v, e); };
+            const S x0 = g(xc);
+            const S hi = tmax(tmax(tmax(g(mx), x0), tmax(g(xm), g(xp))),
+                              tmax(tmax(g(ym), g(yp)), tmax(g(zm), g(zp))));
+            const S lo = tmin(tmin(tmin(g(mn), x0), tmin(g(xm), g(xp))),
+                              tmin(tmin(g(ym), g(yp)), tmin(g(zm), g(zp))));
+            LN::put(his, e, hi);
+            LN::put(los, e, lo);
+            const S axl = upflux(g(xm), x0, g(uL));
+            const S axr = upflux(x0, g(xp), g(uR));
+            const S ayl = upflux(g(ym), x0, g(va));
+            const S ayr = upflux(x0, g(yp), g(vap));
+            const S azl = upflux(g(zm), x0, g(wa));
+            const S azr = upflux(x0, g(zp), g(wap));
             // 2*pos(f) = f + |f| and -2*neg(f) = |f| - f are exact, so these
             // are the oracle's inflow/outflow sums scaled by exactly 2.
-            const T fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) +
+            const S fin2 = (((axl + fabs(axl)) + (fabs(axr) - axr)) +
                             ((ayl + fabs(ayl)) + (fabs(ayr) - ayr))) +
                            ((azl + fabs(azl)) + (fabs(azr) - azr));
-            const T fout2 = (((axr + fabs(axr)) + (fabs(axl) - axl)) +
+            const S fout2 = (((axr + fabs(axr)) + (fabs(axl) - axl)) +
                              ((ayr + fabs(ayr)) + (fabs(ayl) - ayl))) +
                             ((azr + fabs(azr)) + (fabs(azl) - azl));
-            const T di = T(0.5) * fin2 + Eps<T>::value, dou = T(0.5) * fout2 + Eps<T>::value;
+            const S half = LN::cst(T(0.5)), eps = LN::cst(Eps<T>::value);
+            const S di = half * fin2 + eps, dou = half * fout2 + eps;
             if constexpr (sizeof(T) == 8) {
               const T rr2 = rcp(di * dou);
               bu.e[e] = ((hi - x0) * hc.e[e]) * dou * rr2;
               bd.e[e] = ((x0 - lo) * hc.e[e]) * di * rr2;
             } else {
-              bu.e[e] = qdiv((hi - x0) * hc.e[e], di);
-              bd.e[e] = qdiv((x0 - lo) * hc.e[e], dou);
+              LN::put(bu, e, qdiv((hi - x0) * g(hc), di));
+              LN::put(bd, e, qdiv((x0 - lo) * g(hc), dou));
             }
           }
           SST(buA + so, bu);
@@ -1152,8 +1187,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const V bum = SLD(buA + so - L), bdm = SLD(bdA + so - L);
             V res;
 #pragma unroll
-            for (int e = 0; e < K; ++e)
-              res.e[e] = limit_sel(va.e[e], bdm.e[e], bu.e[e], bum.e[e], bd.e[e]);
+            for (int e = 0; e < K; e += PK) {
+              auto g = [e](const V& v) { return LN::get(v, e); };
+              LN::put(res, e, limit_sel(g(va), g(bdm), g(bu), g(bum), g(bd)));
+            }
             SST(vA + so, res);
             if constexpr (MODE == 1) {
               if (keep(t, r)) vstore(a.vo + (q1 + gj[rr]) + sg, res);
@@ -1183,11 +1220,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const V uc = TMU ? tld(tm_u(t) + CW * static_cast<unsigned>(c)) : ucar[c];
             V wres, uls;
 #pragma unroll
-            for (int e = 0; e < K; ++e) {
-              wres.e[e] = limit_sel(wa.e[e], bdkm.e[e], bu.e[e], bukm.e[e], bd.e[e]);
-              const T ul = limit_sel(uc.e[e], bdo.e[e], bu.e[e], buo.e[e], bd.e[e]);
-              uls.e[e] = ul;
-              fxr.e[e] = upflux(xc.e[e], x1.e[e], ul);
+            for (int e = 0; e < K; e += PK) {
+              auto g = [e](const V& v) { return LN::get(v, e); };
+              LN::put(wres, e, limit_sel(g(wa), g(bdkm), g(bu), g(bukm), g(bd)));
+              const S ul = limit_sel(g(uc), g(bdo), g(bu), g(buo), g(bd));
+              LN::put(uls, e, ul);
+              LN::put(fxr, e, upflux(g(xc), g(x1), ul));
             }
             if constexpr (TMWB) {
               tst(tm_w(p1) + CW * static_cast<unsigned>(c), wres);
@@ -1222,14 +1260,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             const V fxl = TMU ? tld(tm_fx() + CW * static_cast<unsigned>(c)) : fxc[c];
             V res;
 #pragma unroll
-            for (int e = 0; e < K; ++e) {
-              const T x0 = xc.e[e];
-              const T fyl = upflux(ym.e[e], x0, vb.e[e]);
-              const T fyr = upflux(x0, yp.e[e], vbp.e[e]);
-              const T fzl = upflux(zm.e[e], x0, wb.e[e]);
-              const T fzr = upflux(x0, zp.e[e], wbp.e[e]);
-              const T div = ((fxr.e[e] - fxl.e[e]) + (fyr - fyl)) + (fzr - fzl);
-              res.e[e] = x0 - qdiv(div, hc.e[e]);
+            for (int e = 0; e < K; e += PK) {
+              auto g = [e](const V& v) { return LN::get(v, e); };
+              const S x0 = g(xc);
+              const S fyl = upflux(g(ym), x0, g(vb));
+              const S fyr = upflux(x0, g(yp), g(vbp));
+              const S fzl = upflux(g(zm), x0, g(wb));
+              const S fzr = upflux(x0, g(zp), g(wbp));
+              const S div = ((g(fxr) - g(fxl)) + (fyr - fyl)) + (fzr - fzl);
+              LN::put(res, e, x0 - qdiv(div, g(hc)));
             }
             const int j = j0 + r - 2;
             if (j < m) vstore(a.out + (q0 + gj[rr]) + sg, res);
@@ -1286,16 +1325,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const V hc = vload<T, K>(a.h + (q0 + gj[rr]) + sg);
         V res;
 #pragma unroll
-        for (int e = 0; e < K; ++e) {
-          const T x0 = xc.e[e];
-          const T fxl = upflux(xm.e[e], x0, ucar[c].e[e]);
-          const T fxr = upflux(x0, xp.e[e], ufresh[c].e[e]);
-          const T fyl = upflux(ym.e[e], x0, vv.e[e]);
-          const T fyr = upflux(x0, yp.e[e], vvp.e[e]);
-          const T fzl = upflux(zm.e[e], x0, ww.e[e]);
-          const T fzr = upflux(x0, zp.e[e], wwp.e[e]);
-          const T div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
-          res.e[e] = x0 - qdiv(div, hc.e[e]);
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          const S x0 = g(xc);
+          const S fxl = upflux(g(xm), x0, g(ucar[c]));
+          const S fxr = upflux(x0, g(xp), g(ufresh[c]));
+          const S fyl = upflux(g(ym), x0, g(vv));
+          const S fyr = upflux(x0, g(yp), g(vvp));
+          const S fzl = upflux(g(zm), x0, g(ww));
+          const S fzr = upflux(x0, g(zp), g(wwp));
+          const S div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
+          LN::put(res, e, x0 - qdiv(div, g(hc)));
         }
         const int j = j0 + r - 1;
         if (j < m) vstore(a.out + (q0 + gj[rr]) + sg, res);
