@@ -1020,6 +1020,24 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           l2_prefetch(f + base, static_cast<unsigned>((pf_rows - first) * L * sizeof(T)));
       }
     }
+#ifndef IMB_M2_PFB  // MODE 2: L2-prefetch the bounds planes the next iteration's bounds phase reads
+#define IMB_M2_PFB 1
+#endif
+    if constexpr (MODE == 2 && !STARC && IMB_M2_PFB) {
+      if (a.pf > 0 && warp == 0 && (lane == 5 || lane == 6)) {
+        const int p = t + 2;  // bounds(t + 1) of the next iteration reads plane t + 2
+        if (p < ie + 1 && p < a.ni + a.R) {
+          const T* f = lane == 5 ? a.mxo : a.mno;
+          const unsigned base = pl(p);
+          const int jb = j0 - C::HALO, nrows = (RR < m ? RR : m);
+          const int j = jb < 0 ? jb + m : jb;
+          const int first = (j + nrows <= m) ? nrows : m - j;
+          l2_prefetch(f + (base + static_cast<unsigned>(j * L)), static_cast<unsigned>(first * L * sizeof(T)));
+          if (first < nrows)
+            l2_prefetch(f + base, static_cast<unsigned>((nrows - first) * L * sizeof(T)));
+        }
+      }
+    }
     IMB_T(0)
     if constexpr (!EARLY) {
       stage_donor(t + lag);  // psi^(1) of the newest plane
