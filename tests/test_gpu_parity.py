@@ -205,7 +205,8 @@ def test_step_host_matches_run_and_reset(orc):
 
 @pytest.mark.parametrize("opts,shape", [(Options(2, True, True), (96, 20, 64)),
                                         (Options(2, False, False), (64, 7, 128)),
-                                        (Options(2, True, False), (200, 13, 32))])
+                                        (Options(2, True, False), (200, 13, 32)),
+                                        (Options(2, True, True), (400, 6, 32))])  # 16 chunks
 def test_pipelined_step_host_is_bit_identical(orc, opts, shape):
     # step_host on a fused shape takes the chunked H2D / kernel / D2H pipeline;
     # it must equal the device-resident run() bit for bit.
