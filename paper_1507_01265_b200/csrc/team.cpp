@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -15,6 +16,17 @@
 #include "imbalance/errors.hpp"
 
 namespace imb::rt {
+
+namespace {
+// NVTX range for Nsight timelines (SURVEY §5 tracing): header-only NVTX v3,
+// a no-op unless a tool injects itself (NVTX_INJECTION64_PATH / nsys / ncu).
+struct Trace {
+  explicit Trace(const char* name) { nvtxRangePushA(name); }
+  ~Trace() { nvtxRangePop(); }
+  Trace(const Trace&) = delete;
+  Trace& operator=(const Trace&) = delete;
+};
+}  // namespace
 
 #define IMB_CUDA(call)                                                                       \
   do {                                                                                       \
@@ -53,6 +65,7 @@ struct NcclApi {
   ncclResult_t (*group_start)() = nullptr;
   ncclResult_t (*group_end)() = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*async_error)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -73,6 +86,7 @@ NcclApi& nccl() {
     api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
     api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+    api.async_error = reinterpret_cast<decltype(api.async_error)>(sym("ncclCommGetAsyncError"));
   });
   if (!api.dl || !api.get_unique_id || !api.comm_init_rank || !api.send || !api.recv ||
       !api.group_start || !api.group_end)
@@ -114,6 +128,13 @@ class NcclLink {
         nccl_check(nccl().recv(p, bytes, ncclUint8, op.peer, comm_, st), "ncclRecv");
     }
     nccl_check(nccl().group_end(), "ncclGroupEnd");
+    // A failed peer or link surfaces asynchronously (the group call itself
+    // returned): poll it so the step throws instead of waiting forever.
+    if (nccl().async_error) {
+      ncclResult_t st = ncclSuccess;
+      nccl_check(nccl().async_error(comm_, &st), "ncclCommGetAsyncError");
+      if (st != ncclSuccess && st != ncclInProgress) nccl_check(st, "NCCL communicator (async)");
+    }
   }
   int nranks() const { return nranks_; }
 
@@ -328,6 +349,7 @@ void Team::exchange_x_self(void* buf) {
 }
 
 void Team::exchange_x_nccl(void* buf) {
+  Trace tr("imb.exchange.nccl");
   IMB_CUDA(cudaEventRecord(ev_ready_, cs_));
   IMB_CUDA(cudaStreamWaitEvent(xs_, ev_ready_, 0));
   nccl_->swap_halos(static_cast<char*>(buf), plane_bytes(), R_, ni_, xs_);
@@ -336,6 +358,7 @@ void Team::exchange_x_nccl(void* buf) {
 }
 
 void Team::exchange_static() {
+  Trace tr("imb.exchange.static");
   for (int f = 0; f < 4; ++f) {
     if (nccl_ && nccl_->nranks() > 1)
       exchange_x_nccl(st_[f]);
@@ -577,6 +600,7 @@ bool Team::graph_step_pair() {
 }
 
 void Team::run(int steps, double* compute_s, double* wall_s) {
+  Trace tr("imb.team.run");
   if (steps < 0) throw ContractError("steps must be >= 0");
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
   IMB_CUDA(cudaSetDevice(device_));
@@ -723,6 +747,7 @@ void Team::step_host_pipelined(const void* x_in, void* x_out) {
 }
 
 void Team::step_host(const void* x_in, void* x_out) {
+  Trace tr("imb.team.step_host");
   halo_fresh_ = false;
   if (left_ || right_) throw ContractError("ring member teams are stepped through their group");
   IMB_CUDA(cudaSetDevice(device_));
@@ -866,6 +891,7 @@ void Team::connect_ipc(const unsigned char* left_blob, const unsigned char* righ
 // epilogue stores the edge planes into the neighbours' step-s buffers
 // (mapped over NVLink), then raise the neighbours' flag words.
 void Team::ipc_step() {
+  Trace tr("imb.team.ipc_step");
   MemOps& ops = memops();
   const std::uint64_t s = step_count_;
   memop_check(ops.wait(cs_, reinterpret_cast<CUdeviceptr>(flags_ + 0), s, CU_STREAM_WAIT_VALUE_GEQ),
