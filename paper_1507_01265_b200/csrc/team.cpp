@@ -691,12 +691,43 @@ void Team::step_host_pipelined(const void* x_in, void* x_out) {
     IMB_CUDA(cudaStreamCreateWithFlags(&ups_, cudaStreamNonBlocking));
     IMB_CUDA(cudaStreamCreateWithFlags(&dns_, cudaStreamNonBlocking));
   }
+  // Chunk boundaries 0 = cut[0] < ... < cut[nch] = ni. Uniform chunks leave
+  // the pipeline's fill (the first chunk's H2D before any kernel) and drain
+  // (the last chunk's D2H after the last kernel) as large as a chunk; the
+  // ramped schedule (default) starts and ends with chunks of `base` planes and
+  // doubles up to `cap` in between, so both ends shrink to a few MB.
   static const int max_chunks = [] {
-    const char* e = std::getenv("IMB_PIPE_CHUNKS");  // A/B knob: chunks per host step
-    return e ? std::max(1, std::atoi(e)) : 16;  // measured: 16 +2.5 % over 8 (C4), 42 worse
+    const char* e = std::getenv("IMB_PIPE_CHUNKS");  // > 0: that many uniform chunks (A/B knob)
+    return e ? std::max(0, std::atoi(e)) : 0;
   }();
-  const int nch = static_cast<int>(
-      std::max<std::int64_t>(1, std::min<std::int64_t>(max_chunks, ni_ / (8 * R_))));
+  std::vector<std::int64_t>& cut = pipe_cuts_;
+  cut.assign(1, 0);
+  static const int base_env = [] {
+    // first/last chunk planes (A/B knob). Measured at C4 (profiles/r02c_e2e_sweep.txt):
+    // ramp from 16 planes 5.51 Gcell/s, uniform 12/16/20/24/32 chunks 5.46/5.48/5.45/5.39/5.26
+    const char* e = std::getenv("IMB_PIPE_BASE");
+    return e ? std::atoi(e) : 16;
+  }();
+  const std::int64_t base = std::max<std::int64_t>(base_env, 2 * R_), cap = std::max<std::int64_t>(base, ni_ / 16);
+  std::vector<std::int64_t> ramp;
+  for (std::int64_t c = base, sum = 0; c < cap && 2 * (sum + c) <= ni_ / 2; c *= 2) {
+    ramp.push_back(c);
+    sum += c;
+  }
+  std::int64_t ramp_sum = 0;
+  for (std::int64_t c : ramp) ramp_sum += c;
+  if (max_chunks > 0 || ramp.empty()) {
+    const std::int64_t n = std::max<std::int64_t>(
+        1, std::min<std::int64_t>(max_chunks > 0 ? max_chunks : 16, ni_ / (8 * R_)));
+    for (std::int64_t c = 1; c <= n; ++c) cut.push_back(ni_ * c / n);
+  } else {
+    for (std::int64_t c : ramp) cut.push_back(cut.back() + c);
+    const std::int64_t mid = ni_ - 2 * ramp_sum, nm = std::max<std::int64_t>(1, (mid + cap - 1) / cap);
+    const std::int64_t m0 = cut.back();
+    for (std::int64_t c = 1; c <= nm; ++c) cut.push_back(m0 + mid * c / nm);
+    for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) cut.push_back(cut.back() + *it);
+  }
+  const int nch = static_cast<int>(cut.size()) - 1;
   while (ev_pipe_.size() < static_cast<std::size_t>(2 * nch + 2)) {
     cudaEvent_t e;
     IMB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -725,7 +756,7 @@ void Team::step_host_pipelined(const void* x_in, void* x_out) {
   IMB_CUDA(cudaEventRecord(ev_edges, ups_));
   std::int64_t done_out = 0;
   for (int c = 0; c < nch; ++c) {
-    const std::int64_t b0 = ni_ * c / nch, b1 = ni_ * (c + 1) / nch;
+    const std::int64_t b0 = cut[c], b1 = cut[c + 1];
     h2d(std::max(b0, R_), std::min(b1, ni_ - R_));
     cudaEvent_t up = ev_pipe_[2 + 2 * c], comp = ev_pipe_[3 + 2 * c];
     IMB_CUDA(cudaEventRecord(up, ups_));

@@ -124,6 +124,7 @@ class Team {
   void step_host_pipelined(const void* x_in, void* x_out);
   cudaStream_t ups_ = nullptr, dns_ = nullptr;  // H2D / D2H copy streams (step_host)
   std::vector<cudaEvent_t> ev_pipe_;
+  std::vector<std::int64_t> pipe_cuts_;  // host-step chunk boundaries (step_host_pipelined)
   template <class T>
   void compute_step_t();
   void* fbuf(int field) const;
