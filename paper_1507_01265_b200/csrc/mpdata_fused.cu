@@ -80,13 +80,20 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #endif
 
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false, int WPR = 1,
-          bool TMWB = false>
+          bool TMWB = false, bool XR = false>
 struct Cfg {
   // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
   static constexpr int KPT = L / (32 * NS * WPR);  // consecutive k per lane and segment
   static_assert(KPT * 32 * NS * WPR == L, "row must split into warp-wide segments");
   static_assert(WPR == 1 || RW == 1, "several warps per row take one row each");
-  static constexpr int RR = NW * RW / WPR;   // region rows
+  // XR: two extra region rows beyond one per warp. Warp w owns row w+1; warp 0
+  // also runs the donor of row 0 and warp NW-1 the donor and the y-face
+  // pseudo-velocity of row RR-1 — the outermost halo rows, which do nothing
+  // else. Without it those two rows idle through the pseudo-velocity and
+  // bounds phases on two of the four schedulers (14 busy warps on 4
+  // schedulers); with it all 16 warps are busy and a tile emits 14 rows
+  // instead of 12 for about the same phase times.
+  static constexpr int RR = NW * RW / WPR + (XR ? 2 : 0);   // region rows
   static constexpr int HALO = NONOS ? 2 : 1; // recomputed rows on each side
   static constexpr int TJ = RR - 2 * HALO;   // output rows per tile
   static constexpr int NT = NW * 32;
@@ -242,6 +249,14 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #define IMB_M2_TMU 1
 #endif
 
+#ifndef IMB_XROWS  // extra halo rows handled by warps 0 and NW-1 (see Cfg::XR)
+#define IMB_XROWS 1
+#endif
+template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR>
+constexpr bool use_xr() {
+  return IMB_XROWS && NONOS && L == 128 && RW == 1 && WPR == 1;
+}
+
 // Instantiations that use tensor memory as per-thread storage: the fp64
 // limiter shapes with one 4-double lane vector per row (see k_fused: the
 // psi^n star ring, the h and v row rings, and TMWB, the z-face velocities and
@@ -372,7 +387,8 @@ __device__ __forceinline__ void tmem_wait_ld(unsigned (&v)[N]) {
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   constexpr bool TMWB = use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
-  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB>;
+  constexpr bool XR = use_xr<T, L, RW, NW, NS, NONOS, WPR>();
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB, XR>;
   static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && WPR == 1 && C::EARLY),
                 "staged inputs: IORD=2 limiter, one row per warp");
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS, SEG = 32 * K;
@@ -412,7 +428,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
 #ifdef IMB_CHECK_SELFTEST  // proves a failing assert traps (tools/checked_build.sh --selftest)
   IMB_ASSERT(blockIdx.x != 0 || threadIdx.x != 0, "selftest", 0);
 #endif
-  const int wrow = (warp / WPR) * RW;              // first region row of this warp
+  const int wrow = (warp / WPR) * RW + (XR ? 1 : 0);  // first region row of this warp
   const int lk = (warp % WPR) * (L / WPR) + lane * K;  // this lane's first k of its segment 0
   const int gs0 = (warp % WPR) * NS;               // row segment index of this warp's segment 0
   // SPLIT: fp64 lanes of 4 consecutive k (one segment). Global rows are read
@@ -437,6 +453,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     gjm[rr] = static_cast<unsigned>((j == 0 ? m - 1 : j - 1) * L + lk);
     gjp[rr] = static_cast<unsigned>((j == m - 1 ? 0 : j + 1) * L + lk);
   }
+  // XR: the extra halo row this warp also handles (-1: none; warp-uniform)
+  const int xrow_r = XR ? (warp == 0 ? 0 : (warp == NW - 1 ? RR - 1 : -1)) : -1;
+  auto xrow_offsets = [&](unsigned& g, unsigned& gm, unsigned& gp) {
+    int j = j0 - C::HALO + xrow_r;
+    j = ((j % m) + m) % m;
+    g = static_cast<unsigned>(j * L + lk);
+    gm = static_cast<unsigned>((j == 0 ? m - 1 : j - 1) * L + lk);
+    gp = static_cast<unsigned>((j == m - 1 ? 0 : j + 1) * L + lk);
+  };
   auto SLD = [](const T* p) {
     if constexpr (SPLIT) return sload_split<T, K, L>(p);
     else return sload<T, K>(p);
@@ -637,16 +662,22 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // the donor's newest plane (nmx_new)
   V nmx_new[NC], nmn_new[NC], nmx[NC], nmn[NC], nmx_mid[NC], nmn_mid[NC];
 
-  // P1: psi^(1) at plane p (donor cell) for all region rows.
-  auto stage_donor = [&](int p) {
+  // P1: psi^(1) at plane p (donor cell) for all region rows: rows rbase..
+  // with element offsets gj_/gjm_/gjp_. OWN: the warp's own rows, which also
+  // keep the psi^n star and fill the TMEM rings; the XR extra row only needs
+  // its psi^(1) in shared memory.
+  auto stage_donor_rows = [&](int p, int rbase, const unsigned* gj_, const unsigned* gjm_,
+                              const unsigned* gjp_, auto own_tag) {
+    constexpr bool OWN = decltype(own_tag)::value;
     const unsigned px = pl(p);
     T* dst = s_x1 + slot3(p) * PL;
     if constexpr (MODE == 2) {  // psi^(2) is an input: stage it, carry the bounds
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
+      for (int c = 0; c < (OWN ? NC : NS); ++c) {
         const int rr = c / NS, so = sgo(c);
-        const unsigned ij = px + gj[rr];
-        SST(dst + (wrow + rr) * L + lks + so, vload<T, K>(a.x + ij + so));
+        const unsigned ij = px + gj_[rr];
+        SST(dst + (rbase + rr) * L + lks + so, vload<T, K>(a.x + ij + so));
+        if constexpr (!OWN) continue;
         if constexpr (STARC) {
           nmx_new[c] = vload<T, K>(a.mxo + ij + so);
           nmn_new[c] = vload<T, K>(a.mno + ij + so);
@@ -655,12 +686,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           tst(tm_h(p) + CW * static_cast<unsigned>(c), vload<T, K>(a.h + ij + so));
         if constexpr (TMC)
           tst2(tm_v(p) + 2 * CW * static_cast<unsigned>(c), vload<T, K>(a.v + ij + so),
-               vload<T, K>(a.v + (px + gjp[rr]) + so));
+               vload<T, K>(a.v + (px + gjp_[rr]) + so));
       }
-      if constexpr (TMH) tmem_wait_st();
+      if constexpr (TMH && OWN) tmem_wait_st();
       return;
     }
-    if constexpr (STG) {
+    if constexpr (STG && OWN) {
       // donors run in plane order: the older two psi^n planes were waited
       // for by the previous donor (all three by the segment's first)
       if (p == ib - 2) {  // (STG implies the limiter: lag 2)
@@ -671,10 +702,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       wait_h(p);
     }
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
+    for (int c = 0; c < (OWN ? NC : NS); ++c) {
       const int rr = c / NS, so = sgo(c);
-      const int r = wrow + rr;
-      const unsigned ij = px + gj[rr];
+      const int r = rbase + rr;
+      const unsigned ij = px + gj_[rr];
       const T* X = a.x + ij + so;
       V xc, xm, xp, ym, yp, zm, zp, hc;
       if constexpr (STG) {
@@ -691,16 +722,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         xc = vload<T, K>(X);
         xm = vload<T, K>(a.x + (ij - PLN) + so);
         xp = vload<T, K>(a.x + (ij + PLN) + so);
-        ym = vload<T, K>(a.x + (px + gjm[rr]) + so);
-        yp = vload<T, K>(a.x + (px + gjp[rr]) + so);
+        ym = vload<T, K>(a.x + (px + gjm_[rr]) + so);
+        yp = vload<T, K>(a.x + (px + gjp_[rr]) + so);
         zm = KMG(c, xc, X);
         zp = KPG(c, xc, X);
         hc = vload<T, K>(a.h + ij + so);
       }
       const V uc = vload<T, K>(a.u + ij + so), up = vload<T, K>(a.u + (ij + PLN) + so);
-      const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp[rr]) + so);
-      if constexpr (TMH) tst(tm_h(p) + CW * static_cast<unsigned>(c), hc);  // h -> [CW c, CW c + CW)
-      if constexpr (TMC) tst2(tm_v(p) + 2 * CW * static_cast<unsigned>(c), vc, vp);  // v rows j, j+1
+      const V vc = vload<T, K>(a.v + ij + so), vp = vload<T, K>(a.v + (px + gjp_[rr]) + so);
+      if constexpr (TMH && OWN) tst(tm_h(p) + CW * static_cast<unsigned>(c), hc);  // h -> [CW c, CW c + CW)
+      if constexpr (TMC && OWN) tst2(tm_v(p) + 2 * CW * static_cast<unsigned>(c), vc, vp);  // v rows j, j+1
       const T* W = a.w + ij + so;
       const V wc = vload<T, K>(W);
       const V wp = KPG(c, wc, W);
@@ -717,7 +748,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         const S fzr = upflux(x0, g(zp), g(wp));
         const S div = ((fxr - fxl) + (fyr - fyl)) + (fzr - fzl);
         LN::put(res, e, x0 - qdiv(div, g(hc)));
-        if constexpr (NONOS && (STARC || TMS)) {
+        if constexpr (NONOS && (STARC || TMS) && OWN) {
           S smx, smn;
           star_minmax(x0, g(xm), g(xp), g(ym), g(yp), g(zm), g(zp), smx, smn);
           LN::put(nmx_new[c], e, smx);
@@ -725,10 +756,94 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       SST(dst + r * L + lks + so, res);
-      if constexpr (TMS)  // segment c -> columns [2CW c, 2CW c + 2CW): max, then min
+      if constexpr (TMS && OWN)  // segment c -> columns [2CW c, 2CW c + 2CW): max, then min
         tst2(tm_star(p) + 2 * CW * static_cast<unsigned>(c), nmx_new[c], nmn_new[c]);
     }
-    if constexpr (TMS) tmem_wait_st();
+    if constexpr (TMS && OWN) tmem_wait_st();
+  };
+  auto stage_donor = [&](int p) {
+    stage_donor_rows(p, wrow, gj, gjm, gjp, std::true_type{});
+    if constexpr (XR) {
+      if (xrow_r >= 0) {  // warps 0 and NW-1: the outermost halo row
+        unsigned xg[1], xgm[1], xgp[1];
+        xrow_offsets(xg[0], xgm[0], xgp[0]);
+        stage_donor_rows(p, xrow_r, xg, xgm, xgp, std::false_type{});
+      }
+    }
+  };
+
+  // XR: the y-face pseudo-velocity between rows RR-2 and RR-1 of plane pb,
+  // run by warp NW-1 after its own row (row RR-1 has no x/z faces). Same
+  // arithmetic as the y-face of stage_pseudo; every operand comes from shared
+  // memory or global memory (the TMEM rings hold the warp's own row).
+  auto pseudo_y_extra = [&](int pb, T* vdst) {
+    const int r = RR - 1;
+    unsigned xg, xgm, xgp;
+    xrow_offsets(xg, xgm, xgp);
+    (void)xgp;
+    const T* s0 = s_x1 + slot3(pb - 1) * PL;
+    const T* s1 = s_x1 + slot3(pb) * PL;
+    const T* s2 = s_x1 + slot3(pb + 1) * PL;
+    const unsigned p1 = pl(pb), p2 = p1 + PLN;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      const int sg = sgo(c);
+      const int so = r * L + lks + sg;
+      const unsigned i1 = p1 + xg, i2 = p2 + xg;
+      const V x1 = SLD(s1 + so);
+      const V a1 = vabs(x1);
+      const V x1m = SLD(s1 + so - L);
+      const V a1m = vabs(x1m);
+      const V a1km = vabs(KMS(c, x1, s1 + so));
+      const V x0 = SLD(s0 + so), x2 = SLD(s2 + so);
+      const V u1c = vload<T, K>(a.u + i1 + sg), u2c = vload<T, K>(a.u + i2 + sg);
+      const T* W1 = a.w + i1 + sg;
+      const V w1 = vload<T, K>(W1);
+      const V v1 = vload<T, K>(a.v + i1 + sg);
+      const V h1c = STG ? sload<T, K>(hrow(pb, r) + sg) : vload<T, K>(a.h + i1 + sg);
+      V bp, bm, cp, cm, Us, Ws;
+      {
+        const V a0m = vabs(SLD(s0 + so - L)), a2m = vabs(SLD(s2 + so - L));
+        const V a1mkp = vabs(KPS(c, x1m, s1 + so - L));
+        const V a1mkm = vabs(KMS(c, x1m, s1 + so - L));
+        const V a1kp = vabs(KPS(c, x1, s1 + so));
+#pragma unroll
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          LN::put(bp, e, g(a2m) + fabs(g(x2)));
+          LN::put(bm, e, g(a0m) + fabs(g(x0)));
+          LN::put(cp, e, g(a1mkp) + g(a1kp));
+          LN::put(cm, e, g(a1mkm) + g(a1km));
+        }
+      }
+      {
+        const V u1m = vload<T, K>(a.u + (p1 + xgm) + sg), u2m = vload<T, K>(a.u + (p2 + xgm) + sg);
+#pragma unroll
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          LN::put(Us, e, (g(u1m) + g(u1c)) + (g(u2m) + g(u2c)));
+        }
+      }
+      {
+        const T* W1m = a.w + (p1 + xgm) + sg;
+        const V w1m = vload<T, K>(W1m);
+        const V w1mkp = KPG(c, w1m, W1m), w1kp = KPG(c, w1, W1);
+#pragma unroll
+        for (int e = 0; e < K; e += PK) {
+          auto g = [e](const V& v) { return LN::get(v, e); };
+          LN::put(Ws, e, (g(w1m) + g(w1)) + (g(w1mkp) + g(w1kp)));
+        }
+      }
+      const V h1m = STG ? sload<T, K>(hrow(pb, r - 1) + sg) : vload<T, K>(a.h + (p1 + xgm) + sg);
+      V res;
+#pragma unroll
+      for (int e = 0; e < K; e += PK) {
+        auto g = [e](const V& v) { return LN::get(v, e); };
+        LN::put(res, e, pseudo_face(g(v1), g(h1m), g(h1c), g(a1), g(a1m), g(bp), g(bm), g(Us), g(cp),
+                                    g(cm), g(Ws)));
+      }
+      SST(vdst + so, res);
+    }
   };
 
   // P2: pseudo-velocities around base plane pb: x-face pb+1 (into ut), y and
@@ -942,6 +1057,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     }
     if constexpr (TMWB) {
       if (!only_u || TMU) tmem_wait_st();
+    }
+    if constexpr (XR) {
+      if (!only_u && warp == NW - 1) pseudo_y_extra(pb, vdst);
     }
   };
 
@@ -1473,7 +1591,8 @@ template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MO
           int WPR = 1>
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR,
-                use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>()>;
+                use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>(),
+                use_xr<T, L, RW, NW, NS, NONOS, WPR>()>;
   auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>;
   // Function attributes and occupancy are per device: configure each device
   // once (a group or a measurement may drive several GPUs from one process).
@@ -1535,7 +1654,9 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
           const char* e = std::getenv("IMB_STG");
           return !(e && e[0] == '0');
         }();
-        if (stg && fs.m >= 18)
+        // (the staged rings copy XROWS rows of a plane in at most two pieces)
+        if (stg && fs.m >= Cfg<T, 128, 1, 16, 1, NONOS, true, 1, false,
+                               use_xr<T, 128, 1, 16, 1, NONOS, 1>()>::XROWS)
           return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE, true>(fs, a, num_sms, st);
       }
 #ifdef IMB_F64_WPR2_NW  // experiment: two warps per row (one 2-double segment per lane)
