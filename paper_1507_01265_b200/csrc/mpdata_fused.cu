@@ -252,6 +252,13 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XROWS  // extra halo rows handled by warps 0 and NW-1 (see Cfg::XR)
 #define IMB_XROWS 1
 #endif
+// XR_DEFER: warp NW-1 computes row RR-1's y-face of plane t+2 right after its
+// donors of plane t+3 (its own rows RR-2 and RR-1 are all it reads), in the
+// donor's phase, where that warp has slack — instead of in the pseudo-velocity
+// phase of plane t+2, where its scheduler would carry 4 1/3 warps of work.
+#ifndef IMB_XR_DEFER
+#define IMB_XR_DEFER 1
+#endif
 template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR>
 constexpr bool use_xr() {
   return IMB_XROWS && NONOS && L == 128 && RW == 1 && WPR == 1;
@@ -1059,7 +1066,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (!only_u || TMU) tmem_wait_st();
     }
     if constexpr (XR) {
-      if (!only_u && warp == NW - 1) pseudo_y_extra(pb, vdst);
+      if (!IMB_XR_DEFER && !only_u && warp == NW - 1) pseudo_y_extra(pb, vdst);
     }
   };
 
@@ -1105,6 +1112,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   }
   __syncthreads();
   stage_pseudo(ib - lag, true, ucar, nullptr, nullptr);
+  if constexpr (XR && IMB_XR_DEFER) {  // the first plane the loop's pseudo phase reads
+    if (warp == NW - 1) pseudo_y_extra(ib - 1, s_v + vws(ib - 1) * PL);
+  }
   if constexpr (sizeof(T) == 4 || L != 128) {
     // Scheduling fence between the warm-up and the streaming loop: measured
     // +12% (fp32) / +10% (l=64 fp64) from the different instruction schedule
@@ -1309,7 +1319,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       if constexpr (TWO) {
-        if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
+        if (t + 3 <= ie + 1) {
+          stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
+          if constexpr (XR && IMB_XR_DEFER) {
+            if (warp == NW - 1) {
+              __syncwarp();  // this warp's psi^(1) rows of plane t+3, lane to lane
+              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL);
+            }
+          }
+        }
       }
       if constexpr (TMWB) tmem_wait_st();
       IMB_T(5)
@@ -1427,7 +1445,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if constexpr (TMWB) tmem_wait_st();
       IMB_T(9)
       if constexpr (EARLY && !TWO) {
-        if (t + 3 <= ie + 1) stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
+        if (t + 3 <= ie + 1) {
+          stage_donor(t + 3);  // the last plane pseudo(ie) reads is ie+1
+          if constexpr (XR && IMB_XR_DEFER) {
+            if (warp == NW - 1) {
+              __syncwarp();  // this warp's psi^(1) rows of plane t+3, lane to lane
+              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL);
+            }
+          }
+        }
       }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
