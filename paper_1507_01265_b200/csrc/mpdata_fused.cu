@@ -254,10 +254,11 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #endif
 // XR_DEFER: warp NW-1 computes row RR-1's y-face of plane t+2 right after its
 // donors of plane t+3 (its own rows RR-2 and RR-1 are all it reads), in the
-// donor's phase, where that warp has slack — instead of in the pseudo-velocity
-// phase of plane t+2, where its scheduler would carry 4 1/3 warps of work.
+// donor's phase — instead of in the pseudo-velocity phase of plane t+2, where
+// its scheduler carries 4 1/3 warps of work. Measured slower (C4 fp64 -2.5 %,
+// fp32 -7.4 %): the donor phase is the longer one for that warp. Off.
 #ifndef IMB_XR_DEFER
-#define IMB_XR_DEFER 1
+#define IMB_XR_DEFER 0
 #endif
 template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR>
 constexpr bool use_xr() {
