@@ -252,6 +252,9 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XROWS  // extra halo rows handled by warps 0 and NW-1 (see Cfg::XR)
 #define IMB_XROWS 1
 #endif
+#ifndef IMB_XR64  // the same for l = 64 rows (two rows per warp, 34 region rows): C2 fp64
+#define IMB_XR64 0  // +0.5 %, fp32 -1.9 % (56-64 spill bytes in fp64); off
+#endif
 // XR_DEFER: warp NW-1 computes row RR-1's y-face of plane t+2 right after its
 // donors of plane t+3 (its own rows RR-2 and RR-1 are all it reads), in the
 // donor's phase — instead of in the pseudo-velocity phase of plane t+2, where
@@ -262,7 +265,7 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #endif
 template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR>
 constexpr bool use_xr() {
-  return IMB_XROWS && NONOS && L == 128 && RW == 1 && WPR == 1;
+  return IMB_XROWS && NONOS && ((L == 128 && RW == 1) || (L == 64 && RW == 2 && IMB_XR64)) && WPR == 1;
 }
 
 // Instantiations that use tensor memory as per-thread storage: the fp64
