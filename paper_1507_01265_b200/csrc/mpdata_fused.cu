@@ -252,6 +252,9 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XROWS  // extra halo rows handled by warps 0 and NW-1 (see Cfg::XR)
 #define IMB_XROWS 1
 #endif
+#ifndef IMB_XR_YWARP  // see stage_pseudo. Split (2): C4 fp64 +2.5 %, C5 fp64 -0.8 %;
+#define IMB_XR_YWARP 2  // all on warp 0 (0): C4 -1.5 %, fp32 -8 % (profiles/r02c_ab_xr_ywarp.txt)
+#endif
 #ifndef IMB_XR64  // the same for l = 64 rows (two rows per warp, 34 region rows): C2 fp64
 #define IMB_XR64 0  // +0.5 %, fp32 -1.9 % (56-64 spill bytes in fp64); off
 #endif
@@ -466,8 +469,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   }
   // XR: the extra halo row this warp also handles (-1: none; warp-uniform)
   const int xrow_r = XR ? (warp == 0 ? 0 : (warp == NW - 1 ? RR - 1 : -1)) : -1;
-  auto xrow_offsets = [&](unsigned& g, unsigned& gm, unsigned& gp) {
-    int j = j0 - C::HALO + xrow_r;
+  auto row_offsets = [&](int r, unsigned& g, unsigned& gm, unsigned& gp) {
+    int j = j0 - C::HALO + r;
     j = ((j % m) + m) % m;
     g = static_cast<unsigned>(j * L + lk);
     gm = static_cast<unsigned>((j == 0 ? m - 1 : j - 1) * L + lk);
@@ -777,7 +780,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     if constexpr (XR) {
       if (xrow_r >= 0) {  // warps 0 and NW-1: the outermost halo row
         unsigned xg[1], xgm[1], xgp[1];
-        xrow_offsets(xg[0], xgm[0], xgp[0]);
+        row_offsets(xrow_r, xg[0], xgm[0], xgp[0]);
         stage_donor_rows(p, xrow_r, xg, xgm, xgp, std::false_type{});
       }
     }
@@ -787,10 +790,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // run by warp NW-1 after its own row (row RR-1 has no x/z faces). Same
   // arithmetic as the y-face of stage_pseudo; every operand comes from shared
   // memory or global memory (the TMEM rings hold the warp's own row).
-  auto pseudo_y_extra = [&](int pb, T* vdst) {
+  auto pseudo_y_extra = [&](int pb, T* vdst, int cbeg, int cend) {
     const int r = RR - 1;
     unsigned xg, xgm, xgp;
-    xrow_offsets(xg, xgm, xgp);
+    // (one-segment rows: only warp NW-1 runs this, whose extra row is RR-1)
+    row_offsets(NS == 1 ? xrow_r : r, xg, xgm, xgp);
     (void)xgp;
     const T* s0 = s_x1 + slot3(pb - 1) * PL;
     const T* s1 = s_x1 + slot3(pb) * PL;
@@ -798,6 +802,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     const unsigned p1 = pl(pb), p2 = p1 + PLN;
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
+      if (NS > 1 && (c < cbeg || c >= cend)) continue;  // warp-uniform
       const int sg = sgo(c);
       const int so = r * L + lks + sg;
       const unsigned i1 = p1 + xg, i2 = p2 + xg;
@@ -1070,7 +1075,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (!only_u || TMU) tmem_wait_st();
     }
     if constexpr (XR) {
-      if (!IMB_XR_DEFER && !only_u && warp == NW - 1) pseudo_y_extra(pb, vdst);
+      if (!IMB_XR_DEFER && !only_u) {
+        // who computes row RR-1's y-face: 0 warp 0 (row 1, whose pseudo phase
+        // has slack), 1 warp NW-1, 2 one segment each (two-segment rows)
+        if constexpr (IMB_XR_YWARP == 2 && NS == 2 && MODE == 0) {  // (IORD=3 passes: -0.8 %)
+          if (warp == 0) pseudo_y_extra(pb, vdst, 0, 1);
+          if (warp == NW - 1) pseudo_y_extra(pb, vdst, 1, 2);
+        } else {
+          if (warp == (IMB_XR_YWARP == 0 ? 0 : NW - 1)) pseudo_y_extra(pb, vdst, 0, NS);
+        }
+      }
     }
   };
 
@@ -1117,7 +1131,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   __syncthreads();
   stage_pseudo(ib - lag, true, ucar, nullptr, nullptr);
   if constexpr (XR && IMB_XR_DEFER) {  // the first plane the loop's pseudo phase reads
-    if (warp == NW - 1) pseudo_y_extra(ib - 1, s_v + vws(ib - 1) * PL);
+    if (warp == NW - 1) pseudo_y_extra(ib - 1, s_v + vws(ib - 1) * PL, 0, NS);
   }
   if constexpr (sizeof(T) == 4 || L != 128) {
     // Scheduling fence between the warm-up and the streaming loop: measured
@@ -1328,7 +1342,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if constexpr (XR && IMB_XR_DEFER) {
             if (warp == NW - 1) {
               __syncwarp();  // this warp's psi^(1) rows of plane t+3, lane to lane
-              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL);
+              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS);
             }
           }
         }
@@ -1454,7 +1468,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if constexpr (XR && IMB_XR_DEFER) {
             if (warp == NW - 1) {
               __syncwarp();  // this warp's psi^(1) rows of plane t+3, lane to lane
-              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL);
+              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS);
             }
           }
         }
