@@ -9,11 +9,11 @@ os.environ["IMB_LIB"] = str(ROOT / "experiments" / "libimb_timing.so")
 sys.path.insert(0, str(ROOT))
 from paper_1507_01265_b200 import _lib, mpdata  # noqa: E402
 lib = _lib.load()
-f = lib.imb_debug_phase_cycles
 buf = (C.c_ulonglong * 320)()
 slots = [(2, "pseudo"), (3, "bar1"), (4, "beta"), (5, "bar2"), (6, "lim+fin"), (8, "donor"),
          (7, "bar3")]
-for n, m, l, fp64 in [(1024, 512, 128, True)]:  # (the counters live in the fp64 object)
+for n, m, l, fp64 in [(1024, 512, 128, True), (1024, 512, 128, False)]:
+    f = lib.imb_debug_phase_cycles if fp64 else lib.imb_debug_phase_cycles_f32
     with mpdata.Team(n, m, l, mpdata.Options(2, True, fp64)) as t:
         t.init_recipe(2, 42)
         t.run(2)

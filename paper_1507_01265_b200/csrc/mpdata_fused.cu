@@ -255,6 +255,9 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XR_YWARP  // see stage_pseudo. Split (2): C4 fp64 +2.5 %, C5 fp64 -0.8 %;
 #define IMB_XR_YWARP 2  // all on warp 0 (0): C4 -1.5 %, fp32 -8 % (profiles/r02c_ab_xr_ywarp.txt)
 #endif
+#ifndef IMB_XR_D17_W0
+#define IMB_XR_D17_W0 1
+#endif
 #ifndef IMB_XR64  // the same for l = 64 rows (two rows per warp, 34 region rows): C2 fp64
 #define IMB_XR64 0  // +0.5 %, fp32 -1.9 % (56-64 spill bytes in fp64); off
 #endif
@@ -402,6 +405,8 @@ template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MO
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   constexpr bool TMWB = use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
   constexpr bool XR = use_xr<T, L, RW, NW, NS, NONOS, WPR>();
+  // XR: row RR-1's donor on warp 0 instead of NW-1 (fp32: phase B balance)
+  constexpr bool XR_D17_W0 = XR && sizeof(T) == 4 && IMB_XR_D17_W0;
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB, XR>;
   static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && WPR == 1 && C::EARLY),
                 "staged inputs: IORD=2 limiter, one row per warp");
@@ -778,7 +783,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   auto stage_donor = [&](int p) {
     stage_donor_rows(p, wrow, gj, gjm, gjp, std::true_type{});
     if constexpr (XR) {
-      if (xrow_r >= 0) {  // warps 0 and NW-1: the outermost halo row
+      if constexpr (XR_D17_W0) {
+        // warp 0 runs both outermost rows' donors (0 and RR-1): its scheduler
+        // has the slack there, warp NW-1's carries row RR-1's y-face
+        if (warp == 0) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int xr = q == 0 ? 0 : RR - 1;
+            unsigned xg[1], xgm[1], xgp[1];
+            row_offsets(xr, xg[0], xgm[0], xgp[0]);
+            stage_donor_rows(p, xr, xg, xgm, xgp, std::false_type{});
+          }
+        }
+      } else if (xrow_r >= 0) {  // warps 0 and NW-1: the outermost halo row
         unsigned xg[1], xgm[1], xgp[1];
         row_offsets(xrow_r, xg[0], xgm[0], xgp[0]);
         stage_donor_rows(p, xrow_r, xg, xgm, xgp, std::false_type{});
@@ -794,7 +811,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     const int r = RR - 1;
     unsigned xg, xgm, xgp;
     // (one-segment rows: only warp NW-1 runs this, whose extra row is RR-1)
-    row_offsets(NS == 1 ? xrow_r : r, xg, xgm, xgp);
+    row_offsets(NS == 1 && !XR_D17_W0 ? xrow_r : r, xg, xgm, xgp);
     (void)xgp;
     const T* s0 = s_x1 + slot3(pb - 1) * PL;
     const T* s1 = s_x1 + slot3(pb) * PL;
@@ -1725,8 +1742,12 @@ bool fused_supported(int iord, int nonos, std::int64_t m, std::int64_t l, std::i
 }
 #endif
 
-#if defined(IMB_PHASE_TIMING) && !defined(IMB_ONLY_F32)
+#if defined(IMB_PHASE_TIMING)
+#ifdef IMB_ONLY_F32
+extern "C" int imb_debug_phase_cycles_f32(unsigned long long* out, int reset) {
+#else
 extern "C" int imb_debug_phase_cycles(unsigned long long* out, int reset) {
+#endif
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
   if (reset) {
     unsigned long long z[10 * 32] = {};
