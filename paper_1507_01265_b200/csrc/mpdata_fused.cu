@@ -255,8 +255,11 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XR_YWARP  // see stage_pseudo. Split (2): C4 fp64 +2.5 %, C5 fp64 -0.8 %;
 #define IMB_XR_YWARP 2  // all on warp 0 (0): C4 -1.5 %, fp32 -8 % (profiles/r02c_ab_xr_ywarp.txt)
 #endif
-#ifndef IMB_XR_D17_W0
-#define IMB_XR_D17_W0 1
+#ifndef IMB_XR_SPLIT_MODES  // bit m: MODE m splits the extra y-face (IORD=3 passes both: -0.8 %)
+#define IMB_XR_SPLIT_MODES 1
+#endif
+#ifndef IMB_XR_D17_W0  // fp32 row RR-1 donor on warp 0: C4 fp32 -6.4 %, C5 -2.4 %; off
+#define IMB_XR_D17_W0 0
 #endif
 #ifndef IMB_XR64  // the same for l = 64 rows (two rows per warp, 34 region rows): C2 fp64
 #define IMB_XR64 0  // +0.5 %, fp32 -1.9 % (56-64 spill bytes in fp64); off
@@ -1095,7 +1098,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (!IMB_XR_DEFER && !only_u) {
         // who computes row RR-1's y-face: 0 warp 0 (row 1, whose pseudo phase
         // has slack), 1 warp NW-1, 2 one segment each (two-segment rows)
-        if constexpr (IMB_XR_YWARP == 2 && NS == 2 && MODE == 0) {  // (IORD=3 passes: -0.8 %)
+        if constexpr (IMB_XR_YWARP == 2 && NS == 2 && ((IMB_XR_SPLIT_MODES >> MODE) & 1)) {
           if (warp == 0) pseudo_y_extra(pb, vdst, 0, 1);
           if (warp == NW - 1) pseudo_y_extra(pb, vdst, 1, 2);
         } else {
