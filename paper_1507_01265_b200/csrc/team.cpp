@@ -7,6 +7,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -745,6 +746,20 @@ void Team::step_host_pipelined(const void* x_in, void* x_out) {
   };
   cudaEvent_t ev_start = ev_pipe_[0], ev_edges = ev_pipe_[1];
   IMB_CUDA(cudaEventRecord(ev_start, cs_));
+  // IMB_PIPE_TRACE=1: per-chunk H2D / kernel / D2H completion times on stderr
+  static const bool trace = [] {
+    const char* e = std::getenv("IMB_PIPE_TRACE");
+    return e && e[0] == '1';
+  }();
+  std::vector<cudaEvent_t> tr;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    IMB_CUDA(cudaEventCreate(&e));
+    IMB_CUDA(cudaEventRecord(e, st));
+    tr.push_back(e);
+  };
+  mark(cs_);
   IMB_CUDA(cudaStreamWaitEvent(ups_, ev_start, 0));
   IMB_CUDA(cudaStreamWaitEvent(dns_, ev_start, 0));
   // edges + periodic self halos
@@ -760,20 +775,33 @@ void Team::step_host_pipelined(const void* x_in, void* x_out) {
     h2d(std::max(b0, R_), std::min(b1, ni_ - R_));
     cudaEvent_t up = ev_pipe_[2 + 2 * c], comp = ev_pipe_[3 + 2 * c];
     IMB_CUDA(cudaEventRecord(up, ups_));
+    mark(ups_);
     IMB_CUDA(cudaStreamWaitEvent(cs_, up, 0));
     const std::int64_t o1 = (c == nch - 1) ? ni_ : std::max(done_out, b1 - R_);
     fused_range(done_out, o1);
     IMB_CUDA(cudaEventRecord(comp, cs_));
+    mark(cs_);
     IMB_CUDA(cudaStreamWaitEvent(dns_, comp, 0));
     if (o1 > done_out)
       IMB_CUDA(cudaMemcpyAsync(out + static_cast<std::size_t>(done_out) * pb, nplane(done_out),
                                static_cast<std::size_t>(o1 - done_out) * pb, cudaMemcpyDeviceToHost,
                                dns_));
+    mark(dns_);
     done_out = o1;
   }
   (void)ev_edges;
   IMB_CUDA(cudaStreamSynchronize(dns_));
   IMB_CUDA(cudaStreamSynchronize(cs_));
+  if (trace) {
+    std::string line = "imb pipe (ms from start: h2d kernel d2h per chunk):";
+    for (std::size_t i = 1; i < tr.size(); ++i) {
+      float ms = 0.f;
+      IMB_CUDA(cudaEventElapsedTime(&ms, tr[0], tr[i]));
+      line += (i % 3 == 1 ? "  | " : " ") + std::to_string(ms).substr(0, 6);
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+    for (cudaEvent_t e : tr) cudaEventDestroy(e);
+  }
   std::swap(x_, xn_);
 }
 
