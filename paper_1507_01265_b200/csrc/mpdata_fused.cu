@@ -272,9 +272,20 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XR_DEFER
 #define IMB_XR_DEFER 0
 #endif
-template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR>
+// bit m: MODE m uses the extra rows. Measured on C5 (profiles/r02c_ab_xr_modes.txt):
+// fp64 without it in MODE 1 (pass 2 of IORD=3, which also stores six fields) +2.1 %;
+// fp32 with it in MODE 0 only +0.3 %.
+#ifndef IMB_XR_MODES_F64
+#define IMB_XR_MODES_F64 5
+#endif
+#ifndef IMB_XR_MODES_F32
+#define IMB_XR_MODES_F32 1
+#endif
+template <class T, int L, int RW, int NW, int NS, bool NONOS, int WPR, int MODE = 0>
 constexpr bool use_xr() {
-  return IMB_XROWS && NONOS && ((L == 128 && RW == 1) || (L == 64 && RW == 2 && IMB_XR64)) && WPR == 1;
+  constexpr int modes = sizeof(T) == 8 ? IMB_XR_MODES_F64 : IMB_XR_MODES_F32;
+  return IMB_XROWS && ((modes >> MODE) & 1) && NONOS &&
+         ((L == 128 && RW == 1) || (L == 64 && RW == 2 && IMB_XR64)) && WPR == 1;
 }
 
 // Instantiations that use tensor memory as per-thread storage: the fp64
@@ -407,7 +418,7 @@ __device__ __forceinline__ void tmem_wait_ld(unsigned (&v)[N]) {
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MODE, bool STG, int WPR>
 __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   constexpr bool TMWB = use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>();
-  constexpr bool XR = use_xr<T, L, RW, NW, NS, NONOS, WPR>();
+  constexpr bool XR = use_xr<T, L, RW, NW, NS, NONOS, WPR, MODE>();
   // XR: row RR-1's donor on warp 0 instead of NW-1 (fp32: phase B balance)
   constexpr bool XR_D17_W0 = XR && sizeof(T) == 4 && IMB_XR_D17_W0;
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB, XR>;
@@ -1656,7 +1667,7 @@ template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MO
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR,
                 use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>(),
-                use_xr<T, L, RW, NW, NS, NONOS, WPR>()>;
+                use_xr<T, L, RW, NW, NS, NONOS, WPR, MODE>()>;
   auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>;
   // Function attributes and occupancy are per device: configure each device
   // once (a group or a measurement may drive several GPUs from one process).
@@ -1720,7 +1731,7 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
         }();
         // (the staged rings copy XROWS rows of a plane in at most two pieces)
         if (stg && fs.m >= Cfg<T, 128, 1, 16, 1, NONOS, true, 1, false,
-                               use_xr<T, 128, 1, 16, 1, NONOS, 1>()>::XROWS)
+                               use_xr<T, 128, 1, 16, 1, NONOS, 1, MODE>()>::XROWS)
           return launch_cfg<T, 128, 1, 16, 1, NONOS, true, MODE, true>(fs, a, num_sms, st);
       }
 #ifdef IMB_F64_WPR2_NW  // experiment: two warps per row (one 2-double segment per lane)
