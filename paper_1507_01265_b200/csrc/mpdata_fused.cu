@@ -261,6 +261,9 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XR_D17_W0  // fp32 row RR-1 donor on warp 0: C4 fp32 -6.4 %, C5 -2.4 %; off
 #define IMB_XR_D17_W0 0
 #endif
+#ifndef IMB_XR_Y0C
+#define IMB_XR_Y0C 1
+#endif
 #ifndef IMB_XR64  // the same for l = 64 rows (two rows per warp, 34 region rows): C2 fp64
 #define IMB_XR64 0  // +0.5 %, fp32 -1.9 % (56-64 spill bytes in fp64); off
 #endif
@@ -422,6 +425,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // XR: row RR-1's donor on warp 0 instead of NW-1 (fp32: phase B balance)
   constexpr bool XR_D17_W0 = XR && sizeof(T) == 4 && IMB_XR_D17_W0;
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB, XR>;
+  // XR_Y0C (two barriers per plane only): row RR-1's y-face of plane t+2 is
+  // computed by warp 0 in the limiter/final phase of iteration t, where warp 0
+  // (region row 1) has nothing else to do; the planes it reads are complete
+  // after the bounds/donor barrier, and its slot row is not read before the
+  // next iteration's bounds phase.
+  constexpr bool XR_Y0C = XR && C::TWO && IMB_XR_Y0C;
   static_assert(!STG || (NONOS && MODE != 2 && RW == 1 && NS == 1 && WPR == 1 && C::EARLY),
                 "staged inputs: IORD=2 limiter, one row per warp");
   constexpr int K = C::KPT, RR = C::RR, PL = C::PLANE, NC = RW * NS, SEG = 32 * K;
@@ -821,11 +830,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // run by warp NW-1 after its own row (row RR-1 has no x/z faces). Same
   // arithmetic as the y-face of stage_pseudo; every operand comes from shared
   // memory or global memory (the TMEM rings hold the warp's own row).
-  auto pseudo_y_extra = [&](int pb, T* vdst, int cbeg, int cend) {
+  // W15: called by warp NW-1 only, whose xrow_r is RR-1 when it owns the
+  // extra donor (the same offsets, computed from the register it has anyway)
+  auto pseudo_y_extra = [&](int pb, T* vdst, int cbeg, int cend, auto w15_tag) {
+    constexpr bool W15 = decltype(w15_tag)::value;
     const int r = RR - 1;
     unsigned xg, xgm, xgp;
-    // (one-segment rows: only warp NW-1 runs this, whose extra row is RR-1)
-    row_offsets(NS == 1 && !XR_D17_W0 ? xrow_r : r, xg, xgm, xgp);
+    row_offsets(W15 && NS == 1 && !XR_D17_W0 ? xrow_r : r, xg, xgm, xgp);
     (void)xgp;
     const T* s0 = s_x1 + slot3(pb - 1) * PL;
     const T* s1 = s_x1 + slot3(pb) * PL;
@@ -1110,10 +1121,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         // who computes row RR-1's y-face: 0 warp 0 (row 1, whose pseudo phase
         // has slack), 1 warp NW-1, 2 one segment each (two-segment rows)
         if constexpr (IMB_XR_YWARP == 2 && NS == 2 && ((IMB_XR_SPLIT_MODES >> MODE) & 1)) {
-          if (warp == 0) pseudo_y_extra(pb, vdst, 0, 1);
-          if (warp == NW - 1) pseudo_y_extra(pb, vdst, 1, 2);
+          if (warp == 0) pseudo_y_extra(pb, vdst, 0, 1, std::false_type{});
+          if (warp == NW - 1) pseudo_y_extra(pb, vdst, 1, 2, std::false_type{});  // (NS == 2: no W15 path)
         } else {
-          if (warp == (IMB_XR_YWARP == 0 ? 0 : NW - 1)) pseudo_y_extra(pb, vdst, 0, NS);
+          if constexpr (IMB_XR_YWARP == 0) {
+            if (warp == 0) pseudo_y_extra(pb, vdst, 0, NS, std::false_type{});
+          } else if constexpr (!XR_Y0C) {
+            if (warp == NW - 1) pseudo_y_extra(pb, vdst, 0, NS, std::true_type{});
+          }
         }
       }
     }
@@ -1161,8 +1176,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   }
   __syncthreads();
   stage_pseudo(ib - lag, true, ucar, nullptr, nullptr);
+  if constexpr (XR_Y0C) {  // the first plane the loop's pseudo phase reads
+    if (warp == 0) pseudo_y_extra(ib - 1, s_v + vws(ib - 1) * PL, 0, NS, std::false_type{});
+  }
   if constexpr (XR && IMB_XR_DEFER) {  // the first plane the loop's pseudo phase reads
-    if (warp == NW - 1) pseudo_y_extra(ib - 1, s_v + vws(ib - 1) * PL, 0, NS);
+    if (warp == NW - 1) pseudo_y_extra(ib - 1, s_v + vws(ib - 1) * PL, 0, NS, std::true_type{});
   }
   if constexpr (sizeof(T) == 4 || L != 128) {
     // Scheduling fence between the warm-up and the streaming loop: measured
@@ -1373,7 +1391,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if constexpr (XR && IMB_XR_DEFER) {
             if (warp == NW - 1) {
               __syncwarp();  // this warp's psi^(1) rows of plane t+3, lane to lane
-              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS);
+              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS, std::true_type{});
             }
           }
         }
@@ -1492,6 +1510,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         }
       }
       if constexpr (TMWB) tmem_wait_st();
+      if constexpr (XR_Y0C) {
+        if (warp == 0 && t + 2 <= ie) pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS, std::false_type{});
+      }
       IMB_T(9)
       if constexpr (EARLY && !TWO) {
         if (t + 3 <= ie + 1) {
@@ -1499,7 +1520,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if constexpr (XR && IMB_XR_DEFER) {
             if (warp == NW - 1) {
               __syncwarp();  // this warp's psi^(1) rows of plane t+3, lane to lane
-              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS);
+              pseudo_y_extra(t + 2, s_v + vws(t + 2) * PL, 0, NS, std::true_type{});
             }
           }
         }

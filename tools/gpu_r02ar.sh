@@ -1,0 +1,7 @@
+#!/bin/bash
+# fp32: row RR-1's y-face on warp 0 in the limiter/final phase (XR_Y0C); parity + A/B
+mkdir -p gpurun_out
+timeout 600 python tools/fp32_check.py > gpurun_out/fp32_check_ar.log 2>&1; echo fp32_check=$?; cat gpurun_out/fp32_check_ar.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_checked.py -x -q -p no:cacheprovider > gpurun_out/pytest_ar.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_ar.log
+python tools/ab.py --fp32 --configs c4,c5s --reps 3 --libs xr4=experiments/libimb_xr4.so,y0c=paper_1507_01265_b200/libimb_b200.so > gpurun_out/ab_ar.txt 2>&1
+cat gpurun_out/ab_ar.txt
