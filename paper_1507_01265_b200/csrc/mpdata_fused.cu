@@ -261,8 +261,8 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XR_D17_W0  // fp32 row RR-1 donor on warp 0: C4 fp32 -6.4 %, C5 -2.4 %; off
 #define IMB_XR_D17_W0 0
 #endif
-#ifndef IMB_XR_Y0C
-#define IMB_XR_Y0C 1
+#ifndef IMB_XR_Y0C  // fp32: C4 -12.3 % (profiles/r02c_ab_xr_y0c.txt) — extra work on warp 0,
+#define IMB_XR_Y0C 0   // which also issues the TMA fills and L2 prefetches, hurts fp32; off
 #endif
 #ifndef IMB_XR64  // the same for l = 64 rows (two rows per warp, 34 region rows): C2 fp64
 #define IMB_XR64 0  // +0.5 %, fp32 -1.9 % (56-64 spill bytes in fp64); off
