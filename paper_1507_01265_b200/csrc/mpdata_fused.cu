@@ -258,6 +258,12 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #ifndef IMB_XR_SPLIT_MODES  // bit m: MODE m splits the extra y-face (IORD=3 passes both: -0.8 %)
 #define IMB_XR_SPLIT_MODES 1
 #endif
+#ifndef IMB_XR_YSPLIT_W1  // the warp taking the second segment of the split extra y-face
+#define IMB_XR_YSPLIT_W1 15
+#endif
+#ifndef IMB_XR_D17_WARP  // the warp that runs row RR-1's donor when IMB_XR_D17_W0
+#define IMB_XR_D17_WARP 0
+#endif
 #ifndef IMB_XR_D17_W0  // fp32 row RR-1 donor on warp 0: C4 fp32 -6.4 %, C5 -2.4 %; off
 #define IMB_XR_D17_W0 0
 #endif
@@ -807,16 +813,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     stage_donor_rows(p, wrow, gj, gjm, gjp, std::true_type{});
     if constexpr (XR) {
       if constexpr (XR_D17_W0) {
-        // warp 0 runs both outermost rows' donors (0 and RR-1): its scheduler
-        // has the slack there, warp NW-1's carries row RR-1's y-face
+        // row RR-1's donor on warp IMB_XR_D17_WARP (fp32: scheduler 0 has the
+        // slack in the bounds/donor phase; warp NW-1 carries row RR-1's y-face)
         if (warp == 0) {
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int xr = q == 0 ? 0 : RR - 1;
-            unsigned xg[1], xgm[1], xgp[1];
-            row_offsets(xr, xg[0], xgm[0], xgp[0]);
-            stage_donor_rows(p, xr, xg, xgm, xgp, std::false_type{});
-          }
+          unsigned xg[1], xgm[1], xgp[1];
+          row_offsets(0, xg[0], xgm[0], xgp[0]);
+          stage_donor_rows(p, 0, xg, xgm, xgp, std::false_type{});
+        }
+        if (warp == IMB_XR_D17_WARP) {
+          unsigned xg[1], xgm[1], xgp[1];
+          row_offsets(RR - 1, xg[0], xgm[0], xgp[0]);
+          stage_donor_rows(p, RR - 1, xg, xgm, xgp, std::false_type{});
         }
       } else if (xrow_r >= 0) {  // warps 0 and NW-1: the outermost halo row
         unsigned xg[1], xgm[1], xgp[1];
@@ -1122,7 +1129,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         // has slack), 1 warp NW-1, 2 one segment each (two-segment rows)
         if constexpr (IMB_XR_YWARP == 2 && NS == 2 && ((IMB_XR_SPLIT_MODES >> MODE) & 1)) {
           if (warp == 0) pseudo_y_extra(pb, vdst, 0, 1, std::false_type{});
-          if (warp == NW - 1) pseudo_y_extra(pb, vdst, 1, 2, std::false_type{});  // (NS == 2: no W15 path)
+          if (warp == IMB_XR_YSPLIT_W1) pseudo_y_extra(pb, vdst, 1, 2, std::false_type{});  // (NS == 2: no W15 path)
         } else {
           if constexpr (IMB_XR_YWARP == 0) {
             if (warp == 0) pseudo_y_extra(pb, vdst, 0, NS, std::false_type{});
