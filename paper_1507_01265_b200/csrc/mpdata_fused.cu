@@ -1660,7 +1660,11 @@ Plan plan_grid(std::int64_t m, int tj, std::int64_t planes, int resident, int wa
   long long best_span = LLONG_MAX;
   const long long min_len = std::max<long long>(1, planes / 256);
   std::vector<long long> slot;
-  for (long long len = planes; len >= min_len; --len) {
+  static const long long max_len = [] {
+    const char* e = std::getenv("IMB_SEG_MAX");  // A/B knob: longest segment in planes
+    return e ? std::max(1LL, std::atoll(e)) : LLONG_MAX;
+  }();
+  for (long long len = std::min<long long>(planes, max_len); len >= min_len; --len) {
     const long long k = planes / len, rem = planes - k * len;
     const long long blocks = ntj * k + (rem > 0 ? ntj : 0);
     if (blocks > 16LL * resident || blocks > INT_MAX / 2) continue;
