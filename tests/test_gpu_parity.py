@@ -365,18 +365,53 @@ def test_group_decomposition_fused_is_bit_identical(shares, opts):
     g.close()
 
 
-@pytest.mark.parametrize("shape", [(5, 18, 128), (7, 19, 128), (16, 47, 128), (6, 130, 128)])
+@pytest.mark.parametrize("shape", [(5, 18, 128), (7, 19, 128), (5, 20, 128), (7, 21, 128),
+                                   (16, 47, 128), (6, 130, 128)])
 @pytest.mark.parametrize("iord", [2, 3])
 def test_fp32_staged_inputs_parity(orc, shape, iord):
     # fp32 at l = 128 stages psi^n and h in shared memory with bulk async copies
-    # (rings refilled one iteration ahead): m = 18 is the smallest staged tile
-    # (rows -1..16 without repeats), short slabs give one- and two-plane
+    # (rings refilled one iteration ahead): with the extra halo rows (18 region
+    # rows) m = 20 is the smallest staged tile (rows -1..18 without repeats) and
+    # m = 18, 19 take the unstaged kernel; short slabs give one- and two-plane
     # segments, m = 130 wraps the last tile's rows.
     opts = Options(iord=iord, nonos=True, fp64=False)
     f = orc.init_fields(2, *shape, seed=31, dtype=np.float32)
     got = gpu_run(f, opts, 3)
     want = oracle_run(orc, f, opts, 3)
     assert rel_err(got, want) <= TOL[False]
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+@pytest.mark.parametrize("shape", [(8, 14, 128), (9, 15, 128), (7, 17, 128), (8, 18, 128),
+                                   (6, 28, 128), (6, 29, 128), (5, 43, 128)])
+def test_extra_row_tiles_parity(orc, fp64, shape):
+    # l = 128 with the limiter runs 18 region rows on 16 warps (14 output rows
+    # per tile; warps 0 and 15 also handle the outermost halo rows): m equal
+    # to, one above, and a little beyond one or two tiles, and m below the 18
+    # region rows (the tile's rows wrap around j).
+    opts = Options(iord=2, nonos=True, fp64=fp64)
+    dt = np.float64 if fp64 else np.float32
+    f = orc.init_fields(2, *shape, seed=37, dtype=dt)
+    got = gpu_run(f, opts, 4)
+    want = oracle_run(orc, f, opts, 4)
+    assert rel_err(got, want) <= TOL[fp64]
+
+
+@pytest.mark.parametrize("shares", [[9, 7, 16], [8, 8, 8, 8]])
+@pytest.mark.parametrize("iord", [2, 3])
+def test_group_extra_rows_fp64_is_bit_identical(shares, iord):
+    # the fp64 l = 128 tiles (extra rows, TMEM rings) under slab decomposition
+    opts = Options(iord, True, True)
+    n, m, l = sum(shares), 31, 128
+    with Team(n, m, l, opts) as t:
+        t.init_recipe(2, 3)
+        t.run(3)
+        single = t.download("x")
+    g = Group(n, m, l, shares, opts=opts)
+    g.init_recipe(2, 3)
+    g.run(3)
+    np.testing.assert_array_equal(g.download("x"), single)
+    g.close()
 
 
 @pytest.mark.parametrize("shares", [[3, 4, 5], [8, 8], [3, 3, 3, 3]])
