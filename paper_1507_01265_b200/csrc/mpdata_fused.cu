@@ -1754,6 +1754,10 @@ int dispatch_l(const FusedShape& fs, const Args<T>& a, int num_sms, cudaStream_t
   constexpr bool D = sizeof(T) == 8;
   switch (fs.l) {
     case 128:
+#ifdef IMB_F32_RW2  // experiment: fp32 with two rows per warp (8 cells per thread, 32-row tiles)
+      if constexpr (!D && NONOS)
+        return launch_cfg<T, 128, 2, 16, 1, NONOS, true, MODE>(fs, a, num_sms, st);
+#endif
       if constexpr (!D && NONOS && MODE != 2) {
         // psi^n and h staged by bulk async copies: C4 fp32 +3.3 %, C5 fp32 +1 %
         // (IMB_STG=0 turns it off for A/B runs)

@@ -42,7 +42,8 @@ def errors(got: np.ndarray, want: np.ndarray, chunk: int = 32) -> dict:
             "bit_identical_frac": same / want.size}
 
 
-def run_config(name: str, steps: int | None = None, threads: int | None = None) -> dict:
+def run_config(name: str, steps: int | None = None, threads: int | None = None,
+               seed: int = 42) -> dict:
     from oracle import oracle as O
     from paper_1507_01265_b200.mpdata import Options, Team
 
@@ -51,7 +52,7 @@ def run_config(name: str, steps: int | None = None, threads: int | None = None) 
     threads = threads or os.cpu_count() or 1
     opts = Options(iord, nonos, fp64)
     with Team(n, m, l, opts) as t:
-        t.init_recipe(recipe, 42)
+        t.init_recipe(recipe, seed)
         fields = [t.download(f) for f in "xuvwh"]
         t0 = time.perf_counter()
         t.run(steps)
@@ -63,7 +64,7 @@ def run_config(name: str, steps: int | None = None, threads: int | None = None) 
     cpu_s = time.perf_counter() - t0
     del fields
     rec = {"config": name, "grid": [n, m, l], "iord": iord, "nonos": nonos,
-           "dtype": "f64" if fp64 else "f32", "steps": steps, "tolerance": TOL[fp64],
+           "dtype": "f64" if fp64 else "f32", "steps": steps, "seed": seed, "tolerance": TOL[fp64],
            "oracle_threads": threads, "oracle_s": round(cpu_s, 2), "gpu_s": round(gpu_s, 3),
            "gpu_launches": launches, "min_ref": float(want.min()), "max_ref": float(want.max())}
     rec.update(errors(got, want))
