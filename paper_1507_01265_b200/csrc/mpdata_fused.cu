@@ -627,6 +627,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // donor(p+2) reuses its slot in the same iteration; h(p) by final(p), before
   // donor(p+3)). Layout: star [0,32) h [32,56) u [56,72) fx [72,80).
   constexpr bool TMU = TMWB && (MODE != 2 || IMB_M2_TMU) && IMB_TMEM_CARRY;
+  // Exact instruction savings of the limited step (round 2, last session; A/B in
+  // profiles/r02f_ab_*.txt). Each knob: -1 = the measured default, 0 = off, 1 = on.
+  //  FLUXST  the limiter stores the limited y/z-face FLUXES of plane t+1 in the velocity
+  //          slots, so the final update reads them instead of forming each flux twice
+  //          (fp64 all modes; fp32 passes 2/3 of IORD=3 only: fp32 MODE 0 measured -1.1 %)
+  //  BCLAMP  beta stored as min(1, beta): the face limits drop their own clamp
+  //          (min(1, a, b) = min(min(1, a), min(1, b)) exactly); fp64
+  //  LFSIGN  a face's limit and its limited flux share the sign test of the velocity; fp64
+  //  KSHARE  (mpdata_math.cuh) the in-lane k pair's max/min feeds both cells' bounds; fp64
+  //          (bit 1; bit 0, the donor's psi^n star, spills: -1.8 %). Alone it is -0.4 % on
+  //          the IORD=3 passes, together with LFSIGN +1.7 % (C5 fp64 13.25 against 13.04)
+#ifndef IMB_FLUXST
+#define IMB_FLUXST -1
+#endif
+#ifndef IMB_BCLAMP
+#define IMB_BCLAMP -1
+#endif
+#ifndef IMB_LFSIGN
+#define IMB_LFSIGN -1
+#endif
+  constexpr bool F64 = sizeof(T) == 8;
+  constexpr bool FLUXST = NONOS && (IMB_FLUXST < 0 ? (F64 || MODE != 0) : IMB_FLUXST != 0);
+  constexpr bool BCLAMP = NONOS && (IMB_BCLAMP < 0 ? F64 : IMB_BCLAMP != 0);
+  constexpr bool LFSIGN = NONOS && PK == 1 && (IMB_LFSIGN < 0 ? F64 : IMB_LFSIGN != 0);
+  constexpr int KSHARE = IMB_KSHARE < 0 ? 2 : IMB_KSHARE;
   __shared__ unsigned s_tmem_base;
   unsigned tm_lane = 0;
   if constexpr (TMM) {
@@ -798,7 +823,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
         LN::put(res, e, x0 - qdiv(div, g(hc)));
         if constexpr (NONOS && (STARC || TMS) && OWN) {
           S smx, smn;
-          star_minmax(x0, g(xm), g(xp), g(ym), g(yp), g(zm), g(zp), smx, smn);
+          if constexpr ((KSHARE & 1) && sizeof(T) == 8 && K == 2) {
+            // (zp[0] = xc[1] and zm[1] = xc[0]: one pair max/min serves both cells)
+            star_minmax_pair(tmax(xc.e[0], xc.e[1]), tmin(xc.e[0], xc.e[1]), e == 0 ? zm.e[0] : zp.e[1],
+                             g(xm), g(xp), g(ym), g(yp), smx, smn);
+          } else {
+            star_minmax(x0, g(xm), g(xp), g(ym), g(yp), g(zm), g(zp), smx, smn);
+          }
           LN::put(nmx_new[c], e, smx);
           LN::put(nmn_new[c], e, smn);
         }
@@ -1341,7 +1372,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             auto g = [e](const V& v) { return LN::get(v, e); };
             const S x0 = g(xc);
             S hi, lo;
-            bound_minmax(g(mx), g(mn), x0, g(xm), g(xp), g(ym), g(yp), g(zm), g(zp), hi, lo);
+            if constexpr ((KSHARE & 2) && sizeof(T) == 8 && K == 2) {
+              bound_minmax_pair(g(mx), g(mn), tmax(xc.e[0], xc.e[1]), tmin(xc.e[0], xc.e[1]),
+                                e == 0 ? zm.e[0] : zp.e[1], g(xm), g(xp), g(ym), g(yp), hi, lo);
+            } else {
+              bound_minmax(g(mx), g(mn), x0, g(xm), g(xp), g(ym), g(yp), g(zm), g(zp), hi, lo);
+            }
             LN::put(his, e, hi);
             LN::put(los, e, lo);
             const S axl = upflux(g(xm), x0, g(uL));
@@ -1374,9 +1410,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               const T rr2 = rcp(di * dou);
               bu.e[e] = ((hi - x0) * hc.e[e]) * dou * rr2;
               bd.e[e] = ((x0 - lo) * hc.e[e]) * di * rr2;
+              if constexpr (BCLAMP) {  // min(1, beta) once per cell instead of once per face limit
+                bu.e[e] = tmin(T(1), bu.e[e]);
+                bd.e[e] = tmin(T(1), bd.e[e]);
+              }
             } else {
-              LN::put(bu, e, qdiv((hi - x0) * g(hc), di));
-              LN::put(bd, e, qdiv((x0 - lo) * g(hc), dou));
+              if constexpr (BCLAMP) {
+                LN::put(bu, e, tmin(LN::cst(T(1)), qdiv((hi - x0) * g(hc), di)));
+                LN::put(bd, e, tmin(LN::cst(T(1)), qdiv((x0 - lo) * g(hc), dou)));
+              } else {
+                LN::put(bu, e, qdiv((hi - x0) * g(hc), di));
+                LN::put(bd, e, qdiv((x0 - lo) * g(hc), dou));
+              }
             }
           }
           SST(buA + so, bu);
@@ -1421,16 +1466,40 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           if (r < 2 || r >= RR - 1) continue;
           const int so = r * L + lks + sg;
           const V bu = SLD(buA + so), bd = SLD(bdA + so);
+          V x1;
+          if constexpr (FLUXST) x1 = SLD(s1 + so);
           {
             const V va = SLD(vA + so);
             const V bum = SLD(buA + so - L), bdm = SLD(bdA + so - L);
             V res;
+            if constexpr (FLUXST) {
+              // the slot keeps the limited y-face FLUX of plane t+1 (both
+              // rows that share the face read it in the next iteration's
+              // final update instead of forming it twice)
+              const V y1m = SLD(s1 + so - L);
+              V fy;
 #pragma unroll
-            for (int e = 0; e < K; e += PK) {
-              auto g = [e](const V& v) { return LN::get(v, e); };
-              LN::put(res, e, limit_sel(g(va), g(bdm), g(bu), g(bum), g(bd)));
+              for (int e = 0; e < K; e += PK) {
+                auto g = [e](const V& v) { return LN::get(v, e); };
+                if constexpr (LFSIGN) {
+                  S vl;
+                  LN::put(fy, e, limit_flux<BCLAMP>(g(va), g(bdm), g(bu), g(bum), g(bd), g(y1m), g(x1), vl));
+                  LN::put(res, e, vl);
+                } else {
+                  const S vl = limit_sel<BCLAMP>(g(va), g(bdm), g(bu), g(bum), g(bd));
+                  LN::put(res, e, vl);
+                  LN::put(fy, e, upflux(g(y1m), g(x1), vl));
+                }
+              }
+              SST(vA + so, fy);
+            } else {
+#pragma unroll
+              for (int e = 0; e < K; e += PK) {
+                auto g = [e](const V& v) { return LN::get(v, e); };
+                LN::put(res, e, limit_sel<BCLAMP>(g(va), g(bdm), g(bu), g(bum), g(bd)));
+              }
+              SST(vA + so, res);
             }
-            SST(vA + so, res);
             if constexpr (MODE == 1) {
               if (keep(t, r)) vstore(a.vo + (q1 + gj[rr]) + sg, res);
             }
@@ -1455,21 +1524,37 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             }
             const V bukm = KMS(c, bu, buA + so), bdkm = KMS(c, bd, bdA + so);
             const V xc = SLD(s0 + so);
-            const V x1 = SLD(s1 + so);
+            if constexpr (!FLUXST) x1 = SLD(s1 + so);
             const V uc = TMU ? tld(tm_u(t) + CW * static_cast<unsigned>(c)) : ucar[c];
-            V wres, uls;
+            V wres, uls, fz;
+            V x1km;
+            if constexpr (FLUXST) x1km = KMS(c, x1, s1 + so);
 #pragma unroll
             for (int e = 0; e < K; e += PK) {
               auto g = [e](const V& v) { return LN::get(v, e); };
-              LN::put(wres, e, limit_sel(g(wa), g(bdkm), g(bu), g(bukm), g(bd)));
-              const S ul = limit_sel(g(uc), g(bdo), g(bu), g(buo), g(bd));
-              LN::put(uls, e, ul);
-              LN::put(fxr, e, upflux(g(xc), g(x1), ul));
+              if constexpr (LFSIGN) {
+                S wl, ul;
+                if constexpr (FLUXST) {
+                  LN::put(fz, e, limit_flux<BCLAMP>(g(wa), g(bdkm), g(bu), g(bukm), g(bd), g(x1km), g(x1), wl));
+                } else {
+                  wl = limit_sel<BCLAMP>(g(wa), g(bdkm), g(bu), g(bukm), g(bd));
+                }
+                LN::put(wres, e, wl);
+                LN::put(fxr, e, limit_flux<BCLAMP>(g(uc), g(bdo), g(bu), g(buo), g(bd), g(xc), g(x1), ul));
+                LN::put(uls, e, ul);
+              } else {
+                const S wl = limit_sel<BCLAMP>(g(wa), g(bdkm), g(bu), g(bukm), g(bd));
+                LN::put(wres, e, wl);
+                if constexpr (FLUXST) LN::put(fz, e, upflux(g(x1km), g(x1), wl));
+                const S ul = limit_sel<BCLAMP>(g(uc), g(bdo), g(bu), g(buo), g(bd));
+                LN::put(uls, e, ul);
+                LN::put(fxr, e, upflux(g(xc), g(x1), ul));
+              }
             }
-            if constexpr (TMWB) {
-              tst(tm_w(p1) + CW * static_cast<unsigned>(c), wres);
+            if constexpr (TMWB) {  // (FLUXST: the limited z-face flux of plane t+1)
+              tst(tm_w(p1) + CW * static_cast<unsigned>(c), FLUXST ? fz : wres);
             } else {
-              SST(wA + so, wres);
+              SST(wA + so, FLUXST ? fz : wres);
             }
             if constexpr (MODE == 1) {
               if (keep(t, r)) {
@@ -1480,8 +1565,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
           if (emit) {
             const V xc = SLD(s0 + so);
-            const V ym = SLD(s0 + so - L), yp = SLD(s0 + so + L);
-            const V zm = KMS(c, xc, s0 + so), zp = KPS(c, xc, s0 + so);
+            V ym, yp, zm, zp;
+            if constexpr (!FLUXST) {
+              ym = SLD(s0 + so - L);
+              yp = SLD(s0 + so + L);
+              zm = KMS(c, xc, s0 + so);
+              zp = KPS(c, xc, s0 + so);
+            }
             const V vb = SLD(vB + so), vbp = SLD(vB + so + L);
             V wb, wbp;
             if constexpr (TMWB) {
@@ -1502,10 +1592,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             for (int e = 0; e < K; e += PK) {
               auto g = [e](const V& v) { return LN::get(v, e); };
               const S x0 = g(xc);
-              const S fyl = upflux(g(ym), x0, g(vb));
-              const S fyr = upflux(x0, g(yp), g(vbp));
-              const S fzl = upflux(g(zm), x0, g(wb));
-              const S fzr = upflux(x0, g(zp), g(wbp));
+              S fyl, fyr, fzl, fzr;
+              if constexpr (FLUXST) {  // the slots hold the limited fluxes themselves
+                fyl = g(vb);
+                fyr = g(vbp);
+                fzl = g(wb);
+                fzr = g(wbp);
+              } else {
+                fyl = upflux(g(ym), x0, g(vb));
+                fyr = upflux(x0, g(yp), g(vbp));
+                fzl = upflux(g(zm), x0, g(wb));
+                fzr = upflux(x0, g(zp), g(wbp));
+              }
               const S div = ((g(fxr) - g(fxl)) + (fyr - fyl)) + (fzr - fzl);
               LN::put(res, e, x0 - qdiv(div, g(hc)));
             }
