@@ -79,8 +79,18 @@ __device__ unsigned long long g_phase_cycles[10 * 32];  // [slot][warp]
 #define IMB_TWO_F64 0
 #endif
 
+// exact instruction savings of the limited step (see k_fused): -1 = measured default
+#ifndef IMB_FLUXST
+#define IMB_FLUXST -1
+#endif
+#ifndef IMB_BCLAMP
+#define IMB_BCLAMP -1
+#endif
+#ifndef IMB_LFSIGN
+#define IMB_LFSIGN -1
+#endif
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG = false, int WPR = 1,
-          bool TMWB = false, bool XR = false>
+          bool TMWB = false, bool XR = false, bool X13 = false>
 struct Cfg {
   // A row is covered by WPR warps, each holding NS segments of 32*KPT cells.
   static constexpr int KPT = L / (32 * NS * WPR);  // consecutive k per lane and segment
@@ -102,7 +112,11 @@ struct Cfg {
   // limiter/final update of plane t (3 barriers per plane instead of 4),
   // which takes a 4th psi^(1) slot.
   static constexpr bool EARLY = NONOS && L == 128;  // l=64: measured -3.5%
-  static constexpr int NX1 = EARLY ? 4 : 3;  // psi^(1) slots
+  // X13 (use_x13): with FLUXST the final update of plane t reads only its own
+  // psi^(1)(t) cells (the limiter stored its y/z fluxes), and the same thread's
+  // donor of plane t+3 comes later in the same phase, so it may overwrite
+  // plane t's slot: three slots again, 18 KB more L1 at l = 128.
+  static constexpr int NX1 = (EARLY && !X13) ? 4 : 3;  // psi^(1) slots
   // TWO: the donor of plane t+3 runs with the bounds (phase 2) and the
   // barrier between the final update (phase 3) and the next plane's
   // pseudo-velocities goes away; a third y/z-velocity slot keeps the next
@@ -296,6 +310,18 @@ constexpr bool use_xr() {
   return IMB_XROWS && ((modes >> MODE) & 1) && NONOS &&
          ((L == 128 && RW == 1) || (L == 64 && RW == 2 && IMB_XR64)) && WPR == 1;
 }
+// Three psi^(1) slots although the donor runs early (Cfg::X13). Needs the
+// stored fluxes (FLUXST, fp64) and the donor in the final update's own phase
+// (not TWO). IMB_X1_3 is a mask over MODE: C4 fp64 28.16 -> 29.10 Gcell/s
+// (+3.3 %); on the IORD=3 passes too, C5 fp64 -1.4 %, so MODE 0 only.
+#ifndef IMB_X1_3
+#define IMB_X1_3 1
+#endif
+template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG, int WPR, int MODE>
+constexpr bool use_x13() {
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
+  return C::EARLY && !C::TWO && sizeof(T) == 8 && IMB_FLUXST != 0 && ((IMB_X1_3 >> MODE) & 1);
+}
 
 // Instantiations that use tensor memory as per-thread storage: the fp64
 // limiter shapes with one 4-double lane vector per row (see k_fused: the
@@ -430,7 +456,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   constexpr bool XR = use_xr<T, L, RW, NW, NS, NONOS, WPR, MODE>();
   // XR: row RR-1's donor on warp 0 instead of NW-1 (fp32: phase B balance)
   constexpr bool XR_D17_W0 = XR && sizeof(T) == 4 && IMB_XR_D17_W0;
-  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB, XR>;
+  using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR, TMWB, XR, use_x13<T, L, RW, NW, NS, NONOS, STG, WPR, MODE>()>;
   // XR_Y0C (two barriers per plane only): row RR-1's y-face of plane t+2 is
   // computed by warp 0 in the limiter/final phase of iteration t, where warp 0
   // (region row 1) has nothing else to do; the planes it reads are complete
@@ -638,20 +664,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   //  KSHARE  (mpdata_math.cuh) the in-lane k pair's max/min feeds both cells' bounds; fp64
   //          (bit 1; bit 0, the donor's psi^n star, spills: -1.8 %). Alone it is -0.4 % on
   //          the IORD=3 passes, together with LFSIGN +1.7 % (C5 fp64 13.25 against 13.04)
-#ifndef IMB_FLUXST
-#define IMB_FLUXST -1
-#endif
-#ifndef IMB_BCLAMP
-#define IMB_BCLAMP -1
-#endif
-#ifndef IMB_LFSIGN
-#define IMB_LFSIGN -1
-#endif
   constexpr bool F64 = sizeof(T) == 8;
   constexpr bool FLUXST = NONOS && (IMB_FLUXST < 0 ? (F64 || MODE != 0) : IMB_FLUXST != 0);
   constexpr bool BCLAMP = NONOS && (IMB_BCLAMP < 0 ? F64 : IMB_BCLAMP != 0);
   constexpr bool LFSIGN = NONOS && PK == 1 && (IMB_LFSIGN < 0 ? F64 : IMB_LFSIGN != 0);
   constexpr int KSHARE = IMB_KSHARE < 0 ? 2 : IMB_KSHARE;
+  static_assert(!(C::EARLY && C::NX1 == 3) || (FLUXST && !C::TWO), "three psi^(1) slots with the early donor need the stored fluxes");
   __shared__ unsigned s_tmem_base;
   unsigned tm_lane = 0;
   if constexpr (TMM) {
@@ -1797,7 +1815,8 @@ template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STARC, int MO
 int launch_cfg(const FusedShape& fs, const Args<T>& proto, int num_sms, cudaStream_t st) {
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR,
                 use_tmwb<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>(),
-                use_xr<T, L, RW, NW, NS, NONOS, WPR, MODE>()>;
+                use_xr<T, L, RW, NW, NS, NONOS, WPR, MODE>(),
+                use_x13<T, L, RW, NW, NS, NONOS, STG, WPR, MODE>()>;
   auto kern = k_fused<T, L, RW, NW, NS, NONOS, STARC, MODE, STG, WPR>;
   // Function attributes and occupancy are per device: configure each device
   // once (a group or a measurement may drive several GPUs from one process).
