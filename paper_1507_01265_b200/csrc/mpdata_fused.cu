@@ -320,7 +320,7 @@ constexpr bool use_xr() {
 template <class T, int L, int RW, int NW, int NS, bool NONOS, bool STG, int WPR, int MODE>
 constexpr bool use_x13() {
   using C = Cfg<T, L, RW, NW, NS, NONOS, STG, WPR>;
-  return C::EARLY && !C::TWO && sizeof(T) == 8 && IMB_FLUXST != 0 && ((IMB_X1_3 >> MODE) & 1);
+  return C::EARLY && !C::TWO && sizeof(T) == 8 && WPR == 1 && IMB_FLUXST != 0 && ((IMB_X1_3 >> MODE) & 1);
 }
 
 // Instantiations that use tensor memory as per-thread storage: the fp64
