@@ -267,10 +267,17 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #define IMB_XROWS 1
 #endif
 #ifndef IMB_XR_YWARP  // see stage_pseudo. Split (2): C4 fp64 +2.5 %, C5 fp64 -0.8 %;
-#define IMB_XR_YWARP 2  // all on warp 0 (0): C4 -1.5 %, fp32 -8 % (profiles/r02c_ab_xr_ywarp.txt)
-#endif
+#define IMB_XR_YWARP 3  // all on warp 0 (0): C4 -1.5 %, fp32 -8 % (profiles/r02c_ab_xr_ywarp.txt);
+#endif                  // four (segment, element) pieces on one warp per scheduler (3): C4 fp64
+                        // +1.3 % over the split (profiles/r02f_ab_xr_y4.txt)
 #ifndef IMB_XR_SPLIT_MODES  // bit m: MODE m splits the extra y-face (IORD=3 passes both: -0.8 %)
 #define IMB_XR_SPLIT_MODES 1
+#endif
+#ifndef IMB_XR_Y4_W0  // IMB_XR_YWARP == 3: the four warps taking one (segment, element) piece each
+#define IMB_XR_Y4_W0 0
+#define IMB_XR_Y4_W1 5
+#define IMB_XR_Y4_W2 10
+#define IMB_XR_Y4_W3 15
 #endif
 #ifndef IMB_XR_YSPLIT_W1  // the warp taking the second segment of the split extra y-face
 #define IMB_XR_YSPLIT_W1 15
@@ -888,7 +895,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
   // memory or global memory (the TMEM rings hold the warp's own row).
   // W15: called by warp NW-1 only, whose xrow_r is RR-1 when it owns the
   // extra donor (the same offsets, computed from the register it has anyway)
-  auto pseudo_y_extra = [&](int pb, T* vdst, int cbeg, int cend, auto w15_tag) {
+  auto pseudo_y_extra = [&](int pb, T* vdst, int cbeg, int cend, auto w15_tag, int ebeg = 0, int eend = C::KPT) {
     constexpr bool W15 = decltype(w15_tag)::value;
     const int r = RR - 1;
     unsigned xg, xgm, xgp;
@@ -952,11 +959,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       V res;
 #pragma unroll
       for (int e = 0; e < K; e += PK) {
+        if (e < ebeg || e >= eend) continue;  // (constants at the call sites: the unused lanes' sums fold away)
         auto g = [e](const V& v) { return LN::get(v, e); };
         LN::put(res, e, pseudo_face(g(v1), g(h1m), g(h1c), g(a1), g(a1m), g(bp), g(bm), g(Us), g(cp),
                                     g(cm), g(Ws)));
       }
-      SST(vdst + so, res);
+      if (ebeg == 0 && eend == K) {
+        SST(vdst + so, res);
+      } else {  // a piece of the vector (IMB_XR_YWARP == 3): element stores
+        if constexpr (!SPLIT && PK == 1) {
+#pragma unroll
+          for (int e = 0; e < K; ++e)
+            if (e >= ebeg && e < eend) vdst[so + e] = res.e[e];
+        }
+      }
     }
   };
 
@@ -1176,7 +1192,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
       if (!IMB_XR_DEFER && !only_u) {
         // who computes row RR-1's y-face: 0 warp 0 (row 1, whose pseudo phase
         // has slack), 1 warp NW-1, 2 one segment each (two-segment rows)
-        if constexpr (IMB_XR_YWARP == 2 && NS == 2 && ((IMB_XR_SPLIT_MODES >> MODE) & 1)) {
+        if constexpr (IMB_XR_YWARP == 3 && NS == 2 && K == 2 && ((IMB_XR_SPLIT_MODES >> MODE) & 1)) {
+          // four pieces (segment, element) on one warp of each scheduler
+          if (warp == IMB_XR_Y4_W0) pseudo_y_extra(pb, vdst, 0, 1, std::false_type{}, 0, 1);
+          if (warp == IMB_XR_Y4_W1) pseudo_y_extra(pb, vdst, 0, 1, std::false_type{}, 1, 2);
+          if (warp == IMB_XR_Y4_W2) pseudo_y_extra(pb, vdst, 1, 2, std::false_type{}, 0, 1);
+          if (warp == IMB_XR_Y4_W3) pseudo_y_extra(pb, vdst, 1, 2, std::false_type{}, 1, 2);
+        } else if constexpr (IMB_XR_YWARP >= 2 && NS == 2 && ((IMB_XR_SPLIT_MODES >> MODE) & 1)) {
           if (warp == 0) pseudo_y_extra(pb, vdst, 0, 1, std::false_type{});
           if (warp == IMB_XR_YSPLIT_W1) pseudo_y_extra(pb, vdst, 1, 2, std::false_type{});  // (NS == 2: no W15 path)
         } else {
