@@ -279,6 +279,8 @@ __device__ __forceinline__ Vec<T, K> kplus_s(const Vec<T, K>& a, const T* p, int
 #define IMB_XR_Y4_W2 10
 #define IMB_XR_Y4_W3 15
 #endif
+// (fp32, one element of the lane's four on each of four warps: C4 fp32 -2.9 … -5.9 %,
+// profiles/r02f_ab_xr_y4_fp32.txt — every piece repeats the row's loads; not kept)
 #ifndef IMB_XR_YSPLIT_W1  // the warp taking the second segment of the split extra y-face
 #define IMB_XR_YSPLIT_W1 15
 #endif
