@@ -549,6 +549,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
     if constexpr (SPLIT) return sload_split<T, K, L>(p);
     else return sload<T, K>(p);
   };
+#ifndef IMB_OUT_CS  // the step's output (the next launch's input) with streaming stores too
+#define IMB_OUT_CS 0  // C4 +-0, C5 fp64 +0.2 %: off
+#endif
+#ifndef IMB_M2_NA  // MODE 2: the bounds fields, read once per cell, bypass L1 allocation
+#define IMB_M2_NA 1  // C5 fp64 +0.7 %, fp32 +-0 (profiles/r02f_ab_cache_policy.txt)
+#endif
+#ifndef IMB_M1_CS  // pass 2 of IORD=3 writes its six intermediate fields with streaming stores
+#define IMB_M1_CS 1  // C5 fp64 +0.7 %, fp32 +-0
+#endif
+  auto ISTORE = [](T* p, const V& v) {  // MODE 1's intermediates (next read by the MODE 2 launch)
+    if constexpr (IMB_M1_CS) vstore_cs(p, v);
+    else vstore(p, v);
+  };
   auto SST = [](T* p, const V& v) {
     if constexpr (SPLIT) sstore_split<T, K, L>(p, v);
     else vstore(p, v);
@@ -1368,8 +1381,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           } else if constexpr (TMS) {  // (warp-uniform here: the whole warp owns row r)
             tld2(tm_star(p1) + 2 * CW * static_cast<unsigned>(c), mx, mn);
           } else if constexpr (MODE == 2) {  // bounds of the previous pass
-            mx = vload<T, K>(a.mxo + i1 + sg);
-            mn = vload<T, K>(a.mno + i1 + sg);
+            if constexpr (IMB_M2_NA) {
+              mx = vload_na<T, K>(a.mxo + i1 + sg);
+              mn = vload_na<T, K>(a.mno + i1 + sg);
+            } else {
+              mx = vload<T, K>(a.mxo + i1 + sg);
+              mn = vload<T, K>(a.mno + i1 + sg);
+            }
           } else {  // psi^n star of plane t+1, reloaded
             const T* N = a.x + i1 + sg;
             const V nc = vload<T, K>(N);
@@ -1473,8 +1491,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
           }
           if constexpr (MODE == 1) {  // bounds for the next pass
             if (keep(t, r)) {
-              vstore(a.mxo + i1 + sg, his);
-              vstore(a.mno + i1 + sg, los);
+              ISTORE(a.mxo + i1 + sg, his);
+              ISTORE(a.mno + i1 + sg, los);
             }
           }
         }
@@ -1543,7 +1561,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               SST(vA + so, res);
             }
             if constexpr (MODE == 1) {
-              if (keep(t, r)) vstore(a.vo + (q1 + gj[rr]) + sg, res);
+              if (keep(t, r)) ISTORE(a.vo + (q1 + gj[rr]) + sg, res);
             }
           }
           if (r >= RR - 2) continue;
@@ -1600,8 +1618,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
             }
             if constexpr (MODE == 1) {
               if (keep(t, r)) {
-                vstore(a.wo + (q1 + gj[rr]) + sg, wres);
-                vstore(a.uo + (q1 + gj[rr]) + sg, uls);
+                ISTORE(a.wo + (q1 + gj[rr]) + sg, wres);
+                ISTORE(a.uo + (q1 + gj[rr]) + sg, uls);
               }
             }
           }
@@ -1650,7 +1668,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused(Args<T> a) {
               LN::put(res, e, x0 - qdiv(div, g(hc)));
             }
             const int j = j0 + r - 2;
-            if (j < m) vstore(a.out + (q0 + gj[rr]) + sg, res);
+            if (j < m) {
+              if constexpr (MODE == 1 || IMB_OUT_CS) ISTORE(a.out + (q0 + gj[rr]) + sg, res);
+              else vstore(a.out + (q0 + gj[rr]) + sg, res);
+            }
           }
           if constexpr (TMU) tst(tm_fx() + CW * static_cast<unsigned>(c), fxr);
           else fxc[c] = fxr;

@@ -107,6 +107,21 @@ __device__ __forceinline__ Vec<T, K> vload(const T* p) {  // global, read-only p
   return r;
 }
 
+// Read-only global load that does not allocate in L1 (data read once per cell).
+template <class T, int K>
+__device__ __forceinline__ Vec<T, K> vload_na(const T* p) {
+  Vec<T, K> r;
+  if constexpr (sizeof(T) == 8 && K == 2) {
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.e[0]), "=d"(r.e[1]) : "l"(p));
+  } else if constexpr (sizeof(T) == 4 && K == 4) {
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(r.e[0]), "=f"(r.e[1]), "=f"(r.e[2]), "=f"(r.e[3]) : "l"(p));
+  } else {
+    r = vload<T, K>(p);
+  }
+  return r;
+}
+
 // Global load through L2 only (coherent with this kernel's own earlier stores).
 template <class T, int K>
 __device__ __forceinline__ Vec<T, K> vload_cg(const T* p) {
@@ -150,6 +165,22 @@ __device__ __forceinline__ Vec<T, K> sload(const T* p) {  // shared
     r.e[0] = p[0];
   }
   return r;
+}
+
+// Global store with the evict-first (streaming) policy: for fields that are
+// written once and next read by another launch, long after L2 has turned over.
+template <class T, int K>
+__device__ __forceinline__ void vstore_cs(T* p, const Vec<T, K>& v) {
+  if constexpr (sizeof(T) == 8 && K == 2) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v.e[0], v.e[1]));
+  } else if constexpr (sizeof(T) == 4 && K == 4) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v.e[0], v.e[1], v.e[2], v.e[3]));
+  } else if constexpr (sizeof(T) == 4 && K == 2) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v.e[0], v.e[1]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < K; ++e) __stcs(p + e, v.e[e]);
+  }
 }
 
 template <class T, int K>
